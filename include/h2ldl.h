@@ -1,0 +1,144 @@
+/*
+ * h2ldl.h — C ABI of libh2ldl.so, the B200 (sm_100a) generalized-LDL^T
+ * inertia engine for rank-structured (BLR2 / HSS / H2) symmetric matrices.
+ *
+ * This is the drop-in boundary for the reference's hot path:
+ *
+ *   h2l_inertia       replaces  gldl.generalized_ldl / gldl.inertia
+ *                               (/root/reference/pkg/src/h2slice/gldl.py:605-633)
+ *                               for s shifts at once; the Python shims in
+ *                               paper_2311_08618_b200/ldl.py keep the retry
+ *                               loop (gldl.py:615-633) and exceptions.
+ *   h2l_upload        replaces  the per-origin skeleton caches
+ *                               RankStructuredMatrix.skeleton_diag/_offdiag
+ *                               (compress.py:99-127): the payload is uploaded
+ *                               once and Q^T A Q is formed on the device.
+ *   h2l_bk_factor     replaces  the native operator plug-in
+ *                               _core.bk_factor (_core/_kernels.pyx:21-125),
+ *                               bit-identical packed output and ipiv.
+ *   h2l_bk_inertia    replaces  _core.bk_inertia (_kernels.pyx:128-168).
+ *
+ * Conventions
+ *  - Every function returns H2L_OK (0) or a negative H2L_E* code; the last
+ *    message is available from h2l_last_error(engine) (engine may be NULL for
+ *    the engine-less entry points).
+ *  - All matrices are row-major (C order) float64; host buffers are owned by
+ *    the caller, device memory by the engine.  Calls are synchronous.
+ *  - An engine is bound to one CUDA device and one stream; calls on one engine
+ *    are not re-entrant.  Distinct engines may be driven from distinct host
+ *    threads.
+ *  - No C++ exception crosses this boundary; no CPU fallback exists: without
+ *    a usable sm_100 device every compute entry point returns H2L_ENODEV.
+ */
+#ifndef H2LDL_H
+#define H2LDL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    H2L_OK = 0,
+    H2L_EINVAL = -1,   /* bad argument / inconsistent plan */
+    H2L_ENODEV = -2,   /* no CUDA device / not sm_100 */
+    H2L_ECUDA = -3,    /* CUDA runtime error */
+    H2L_ENOMEM = -4,   /* device allocation failed */
+    H2L_ESTATE = -5    /* call order violated (e.g. inertia before upload) */
+};
+
+/* per-shift status written by h2l_inertia */
+enum {
+    H2L_SHIFT_OK = 0,          /* factored; counts valid (zero count may be > 0) */
+    H2L_SHIFT_SINGULAR = 1     /* a BK pivot block was singular (reference: ShiftHitEigenvalue) */
+};
+
+/* structure kinds: reference BlockStructure.kind (partition.py:122-157) */
+enum { H2L_STRONG = 0, H2L_WEAK = 1, H2L_FLAT = 2 };
+
+typedef struct h2l_engine h2l_engine;
+
+/*
+ * Static schedule + payload of one unshifted RankStructuredMatrix
+ * (compress.py:24-56).  Clusters are numbered level-major: node id of
+ * (level, i) is (1 << level) - 1 + i.  Offsets index `arena` (doubles).
+ */
+typedef struct h2l_plan {
+    int32_t n;            /* matrix order */
+    int32_t depth;        /* tree depth; leaves at level `depth` */
+    int32_t kind;         /* H2L_STRONG / H2L_WEAK / H2L_FLAT */
+    int32_t n_dense;      /* inadmissible leaf pairs (i < j) */
+    int32_t n_lowrank;    /* classified low-rank pairs, all levels */
+    int32_t n_deferred;   /* deferred non-leaf pairs, all levels */
+    double eps;           /* construction tolerance; drop_tol = eps*(scale0+|mu|) */
+    double scale0;        /* max |entry| of the leaf diagonal blocks (compress.py:71-82) */
+    const int64_t *ranges;      /* [nodes][2]: index range [start, stop) */
+    const int32_t *dense;       /* [n_dense][2] leaf cluster pairs */
+    const int32_t *lowrank;     /* [n_lowrank][3] (level, i, j) */
+    const int32_t *deferred;    /* [n_deferred][3] (level, i, j) */
+    const int32_t *basis_rank;  /* [nodes] skeleton rank, -1 when the node has no basis */
+    const int32_t *basis_dim;   /* [nodes] rows of the square basis [U_R | U_S] */
+    const int64_t *basis_off;   /* [nodes] arena offset of [U_R | U_S] (dim x dim), -1 none */
+    const int64_t *diag_off;    /* [leaves] arena offset of leaf_diag[i] (m_i x m_i) */
+    const int64_t *dense_off;   /* [n_dense] arena offset of leaf_offdiag (m_i x m_j) */
+    const int64_t *lowrank_off; /* [n_lowrank] arena offset of the coupling (r_i x r_j) */
+    const double *arena;        /* all float64 payload */
+    int64_t arena_len;          /* doubles in arena */
+} h2l_plan;
+
+/* structural statistics of the last h2l_inertia call (gldl.py:189-195) */
+typedef struct h2l_stats {
+    int64_t fill_blocks;
+    int64_t recompressions;
+    int64_t rank_added;
+    int64_t max_front;
+    double dropped_fro;   /* summed over shifts */
+    double flops;         /* algorithmic fp64 flops of the call (all shifts) */
+    double bytes;         /* algorithmic HBM bytes of the call (all shifts) */
+    double ms_total;      /* device time of the call (CUDA events) */
+    double ms_schur;      /* device time inside the Schur-update GEMM launches */
+    double ms_bk;         /* device time inside the BK launches */
+    int64_t launches;     /* kernels launched by the call */
+    double schur_flops;   /* flops of the Schur-update GEMM launches */
+} h2l_stats;
+
+int h2l_create(h2l_engine **engine, int device);
+int h2l_destroy(h2l_engine *engine);
+const char *h2l_last_error(const h2l_engine *engine);
+
+/* Upload the payload and build the shift-independent skeleton blocks. */
+int h2l_upload(h2l_engine *engine, const h2l_plan *plan);
+
+/*
+ * Inertia of (A - mu[z] I) for z < s, all shifts in one batched sweep.
+ * counts: [s][3] (neg, zero, pos); status: [s] H2L_SHIFT_*.
+ * stats may be NULL.
+ */
+int h2l_inertia(h2l_engine *engine, const double *mu, int32_t s, int64_t *counts,
+                int32_t *status, h2l_stats *stats);
+
+/* Tuning knobs (key, value): "max_batch" shifts per device wave (default 64). */
+int h2l_set_option(h2l_engine *engine, const char *key, int64_t value);
+
+/*
+ * Batched Bunch-Kaufman LDL^T on the device, the reference kernel's contract
+ * (_kernels.pyx:21-125): `count` n x n row-major matrices in `a` (host,
+ * overwritten with the packed factor, lower triangle), ipiv [count][n],
+ * tol [count], info [count] (0 or k+1).  Bit-identical to the reference.
+ */
+int h2l_bk_factor(int device, double *a, int64_t n, int32_t count, int64_t *ipiv,
+                  const double *tol, int64_t *info);
+
+/* (neg, zero, pos) of packed BK factors, _kernels.pyx:128-168; counts [count][3]. */
+int h2l_bk_inertia(int device, const double *a, int64_t n, int32_t count, const int64_t *ipiv,
+                   const double *zero_tol, int64_t *counts);
+
+/* Library version string, e.g. "h2ldl 0.1 sm_100a". */
+const char *h2l_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* H2LDL_H */

@@ -1,0 +1,99 @@
+// Shared declarations of the sm_100a kernels behind libh2ldl.so.
+//
+// Every kernel is "batched twice": over a host-built task list (the blocks
+// of one elimination step / merge) and over shifts (gridDim.y = s).  A task
+// stores the pointers of shift 0 plus a per-operand shift stride, so one
+// launch advances every shift of the wave (shift batching).
+// All matrices are row-major float64.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace h2l {
+
+// dst = (acc ? dst : 0) + alpha * op(src) - [shift_diag] mu[z] * I   (rows x cols)
+// src == nullptr -> zero fill (identity when ident != 0).
+struct CopyTask {
+    const double *src;
+    double *dst;
+    int64_t sstride, dstride;  // per-shift strides (elements)
+    int rows, cols;
+    int lds, ldd;
+    int trans;                 // element (r, c) = src[c*lds + r]
+    int acc;
+    int ident;
+    int shift_diag;
+    double alpha;
+};
+
+// C = alpha * opA(MxK) * opB(KxN) + beta * C
+//   opA: tA=0 A[m*lda+k], tA=1 A[k*lda+m];  opB: tB=0 B[k*ldb+n], tB=1 B[n*ldb+k]
+struct GemmTask {
+    const double *A;
+    const double *B;
+    double *C;
+    int64_t sA, sB, sC;
+    int M, N, K;
+    int lda, ldb, ldc;
+    int tA, tB;
+    double alpha, beta;
+};
+
+constexpr int PANEL_ROWS = 32;
+
+// one <= 32-row tile of the elimination panel (k_panel.cu)
+struct PanelTile {
+    const double *src;
+    int64_t sstride;
+    int lds;
+    int trans;       // panel row r = column (src_row0 + r) of src
+    int row0;        // first panel row of the tile
+    int nrows;
+    int src_row0;
+    int pad;
+};
+
+// Engine-mode BK job: factor the leading n x n block of a (row-major, ld).
+struct BkJob {
+    double *a;
+    int64_t astride;
+    int ld;
+    int n;
+    int *perm;       // [shift][pstride]
+    double *dinfo;   // [shift][3*pstride]: d, e (2x2 off-diagonal), block size
+    int64_t pstride;
+};
+
+// ---- launchers (stream-ordered; return the launch error)
+int copy_tiles(int rows, int cols);
+void launch_copy_prefixed(const CopyTask *dev_tasks, const int *dev_prefix, int ntasks,
+                          int total_tiles, int nshift, const double *mu, cudaStream_t st);
+
+int gemm_tiles(int M, int N);
+void launch_gemm(const GemmTask *dev_tasks, const int *dev_tile_prefix, int ntasks,
+                 int total_tiles, int nshift, cudaStream_t st);
+
+int64_t bk_scratch_doubles(int n);
+cudaError_t launch_bk_engine(const BkJob *dev_jobs, int njobs, int nshift, int nmax,
+                             int64_t *counts, int *status, double *scratch,
+                             int64_t scratch_stride, cudaStream_t st);
+cudaError_t launch_bk_kat(double *a, int n, int count, const double *tol, int64_t *ipiv,
+                          int64_t *info, double *scratch, cudaStream_t st);
+cudaError_t launch_bk_inertia(const double *a, int n, int count, const int64_t *ipiv,
+                              const double *zero_tol, int64_t *counts, cudaStream_t st);
+
+cudaError_t launch_panel(const PanelTile *dev_tiles, int ntiles, int nshift, const double *L,
+                         int64_t lstride, int ldl, int n, const int *perm, const double *dinfo,
+                         int64_t pstride, double *W, double *X, int64_t wstride, int ldw,
+                         cudaStream_t st);
+
+cudaError_t launch_pqr(double *GT, int64_t gstride, int c, int nR, int ldg, double *tau, int *piv,
+                       int *used, double *norms, int64_t vstride, int64_t cstride,
+                       const double *tol, int *rank, double *dropped, const int *active,
+                       int target, int nshift, cudaStream_t st);
+cudaError_t launch_form_tr(const double *GT, int64_t gstride, int ldg, const double *tau,
+                           const int *piv, int64_t vstride, int nR, int t, double *Tr,
+                           int64_t tstride, const int *active, int nshift, cudaStream_t st);
+
+}  // namespace h2l

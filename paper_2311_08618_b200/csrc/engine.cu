@@ -1,0 +1,1270 @@
+// Host orchestration of the level-by-level generalized LDL^T (the hot path)
+// and the C ABI of libh2ldl.so (include/h2ldl.h).
+//
+// Algorithm: the reference engine `_Engine` (gldl.py:179-602), re-expressed
+// as a sequence of batched device launches.  For one wave of s shifts the
+// engine keeps, per cluster of the current level, s-batched device blocks:
+//   diag[i]  m_i x m_i          (gldl.py:229-256)
+//   offd(i,j) m_i x m_j  i<j    dense near field / deferred pairs
+//   coup(i,j) rS_i x rS_j       skeleton couplings of low-rank pairs
+//   fill(i,j) m_i x m_j         fill-in created by elimination
+// and walks the reference's schedule: per level, clusters ascending:
+// recompress(i) -> eliminate(i); fold fills into couplings; merge to
+// parents; BK of the root.  Every step is one or a few launches over all
+// blocks it touches and all shifts of the wave.
+//
+// Shift batching (north star (b)): the structure (which blocks exist and
+// their dimensions) is shared by all shifts of a wave.  The only
+// data-dependent structure is the recompression rank t; the wave uses
+// t = max over its shifts, each shift rotating with its own reflectors -
+// a shift then keeps >= the directions the reference keeps, i.e. it is at
+// least as accurate, and the inertia is unchanged for shifts farther than
+// the construction tolerance from the spectrum.
+//
+// Live-row rule: a partner eliminated earlier in the level only contributes
+// its skeleton rows to the panel and only its skeleton rows are updated -
+// the reference carries its (exactly zero) redundant rows through the
+// products (gldl.py:365-409); skipping them changes no value.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "../../include/h2ldl.h"
+
+namespace h2l {
+
+struct CudaFail : std::runtime_error {
+    int code;
+    CudaFail(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(x)                                                                              \
+    do {                                                                                   \
+        cudaError_t e_ = (x);                                                              \
+        if (e_ != cudaSuccess)                                                             \
+            throw ::h2l::CudaFail(e_ == cudaErrorMemoryAllocation ? H2L_ENOMEM : H2L_ECUDA,       \
+                           std::string(#x) + ": " + cudaGetErrorString(e_));                \
+    } while (0)
+
+using Pair = std::pair<int, int>;
+
+static inline int64_t pad4(int64_t v) { return (v + 3) / 4 * 4; }
+
+// s-batched device block (row-major, ld = cols)
+struct Blk {
+    double *p = nullptr;
+    int rows = 0, cols = 0;
+    int64_t bs = 0;
+    double *at(int r, int c) const { return p + (int64_t)r * cols + c; }
+};
+
+// linear host(pinned)->device staging of task lists; reset at stream syncs
+struct Staging {
+    char *h = nullptr, *d = nullptr;
+    size_t cap = 0, off = 0;
+    void init(size_t bytes) {
+        cap = bytes;
+        CK(cudaMallocHost(&h, cap));
+        CK(cudaMalloc(&d, cap));
+    }
+    void release() {
+        if (h) cudaFreeHost(h);
+        if (d) cudaFree(d);
+        h = d = nullptr;
+    }
+};
+
+struct Cl {
+    int m = 0, nR = 0, nS = 0, r0 = 0;
+};
+
+class Engine {
+public:
+    explicit Engine(int device) : dev_(device) {
+        CK(cudaSetDevice(dev_));
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, dev_));
+        if (prop.major < 10) throw CudaFail(H2L_ENODEV, "device is not sm_100 class");
+        CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, dev_));
+        uint64_t thr = UINT64_MAX;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        stage_.init(size_t(64) << 20);
+        for (int k = 0; k < 2; ++k) CK(cudaEventCreate(&ev_call_[k]));
+    }
+    ~Engine() {
+        cudaSetDevice(dev_);
+        cudaStreamSynchronize(st_);
+        free_payload();
+        for (auto &e : ev_pool_) cudaEventDestroy(e);
+        for (int k = 0; k < 2; ++k) cudaEventDestroy(ev_call_[k]);
+        stage_.release();
+        cudaStreamDestroy(st_);
+    }
+
+    void set_option(const std::string &k, int64_t v) {
+        if (k == "max_batch") max_batch_ = (int)std::max<int64_t>(1, v);
+        else if (k == "time_kernels") time_kernels_ = v != 0;
+        else throw CudaFail(H2L_EINVAL, "unknown option " + k);
+    }
+
+    // ------------------------------------------------------------------ upload
+    void upload(const h2l_plan *pl) {
+        CK(cudaSetDevice(dev_));
+        free_payload();
+        if (!pl || pl->n <= 0 || pl->depth < 0 || pl->depth > 30)
+            throw CudaFail(H2L_EINVAL, "invalid plan header");
+        n_ = pl->n;
+        depth_ = pl->depth;
+        kind_ = pl->kind;
+        eps_ = pl->eps;
+        scale0_ = pl->scale0;
+        const int nodes = (1 << (depth_ + 1)) - 1;
+        ranges_.assign(pl->ranges, pl->ranges + 2 * nodes);
+        brank_.assign(pl->basis_rank, pl->basis_rank + nodes);
+        bdim_.assign(pl->basis_dim, pl->basis_dim + nodes);
+        boff_.assign(pl->basis_off, pl->basis_off + nodes);
+        dense_.clear();
+        for (int e = 0; e < pl->n_dense; ++e) dense_.push_back({pl->dense[2 * e], pl->dense[2 * e + 1]});
+        lowrank_.clear();
+        deferred_.clear();
+        coup_off_.clear();
+        for (int e = 0; e < pl->n_lowrank; ++e) {
+            int l = pl->lowrank[3 * e], i = pl->lowrank[3 * e + 1], j = pl->lowrank[3 * e + 2];
+            lowrank_[l].push_back({i, j});
+            coup_off_[{l, i * 1000003LL + j}] = pl->lowrank_off[e];
+        }
+        for (int e = 0; e < pl->n_deferred; ++e)
+            deferred_[pl->deferred[3 * e]].push_back({pl->deferred[3 * e + 1], pl->deferred[3 * e + 2]});
+        CK(cudaMalloc(&arena_, sizeof(double) * std::max<int64_t>(1, pl->arena_len)));
+        CK(cudaMemcpy(arena_, pl->arena, sizeof(double) * pl->arena_len, cudaMemcpyHostToDevice));
+        const int L = depth_;
+        const int nleaf = 1 << L;
+        // ---- skeleton prologue (K1): S = Q^T A Q, shift independent (compress.py:99-127)
+        int64_t tot = 0;
+        std::vector<int64_t> doff(nleaf), ooff(dense_.size());
+        for (int i = 0; i < nleaf; ++i) { doff[i] = tot; tot += pad4((int64_t)lsize(i) * lsize(i)); }
+        for (size_t e = 0; e < dense_.size(); ++e) {
+            ooff[e] = tot;
+            tot += pad4((int64_t)lsize(dense_[e].first) * lsize(dense_[e].second));
+        }
+        CK(cudaMalloc(&skel_, sizeof(double) * std::max<int64_t>(1, tot)));
+        double *tmp = nullptr;
+        int64_t tmpn = 0;
+        for (int i = 0; i < nleaf; ++i) tmpn = std::max<int64_t>(tmpn, (int64_t)lsize(i) * lsize(i));
+        for (auto &pr : dense_)
+            tmpn = std::max<int64_t>(tmpn, (int64_t)lsize(pr.first) * lsize(pr.second));
+        CK(cudaMalloc(&tmp, sizeof(double) * std::max<int64_t>(1, tmpn * 1)));
+        skel_diag_.assign(nleaf, nullptr);
+        skel_off_.clear();
+        // one block at a time (prologue runs once per H; simplicity over speed)
+        for (int i = 0; i < nleaf; ++i) {
+            const int m = lsize(i);
+            skel_diag_[i] = skel_ + doff[i];
+            if (m == 0) continue;
+            const double *A = arena_ + pl->diag_off[i];
+            congruence(A, m, m, leaf_basis(i), leaf_basis(i), skel_diag_[i], tmp);
+        }
+        for (size_t e = 0; e < dense_.size(); ++e) {
+            const int i = dense_[e].first, j = dense_[e].second;
+            double *dst = skel_ + ooff[e];
+            skel_off_[dense_[e]] = dst;
+            congruence(arena_ + pl->dense_off[e], lsize(i), lsize(j), leaf_basis(i), leaf_basis(j),
+                       dst, tmp);
+        }
+        CK(cudaStreamSynchronize(st_));
+        stage_.off = 0;
+        cudaFree(tmp);
+        uploaded_ = true;
+    }
+
+    // ----------------------------------------------------------------- inertia
+    void inertia(const double *mu, int s, int64_t *counts, int32_t *status, h2l_stats *stats) {
+        if (!uploaded_) throw CudaFail(H2L_ESTATE, "h2l_inertia before h2l_upload");
+        CK(cudaSetDevice(dev_));
+        h2l_stats acc{};
+        CK(cudaEventRecord(ev_call_[0], st_));
+        for (int w0 = 0; w0 < s; w0 += max_batch_) {
+            const int ws = std::min(max_batch_, s - w0);
+            run_wave(mu + w0, ws, counts + 3 * (int64_t)w0, status + w0, acc);
+        }
+        CK(cudaEventRecord(ev_call_[1], st_));
+        CK(cudaEventSynchronize(ev_call_[1]));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev_call_[0], ev_call_[1]));
+        acc.ms_total = ms;
+        if (stats) *stats = acc;
+    }
+
+    std::string err;
+
+private:
+    int dev_;
+    cudaStream_t st_ = nullptr;
+    Staging stage_;
+    int max_batch_ = 64;
+    bool time_kernels_ = false;
+    bool uploaded_ = false;
+    cudaEvent_t ev_call_[2];
+    std::vector<cudaEvent_t> ev_pool_;
+    size_t ev_used_ = 0;
+    std::vector<std::pair<int, double>> ev_marks_;  // (event index of start, kind)
+
+    // plan
+    int n_ = 0, depth_ = 0, kind_ = 0;
+    double eps_ = 0, scale0_ = 0;
+    std::vector<int64_t> ranges_, boff_;
+    std::vector<int> brank_, bdim_;
+    std::vector<Pair> dense_;
+    std::map<int, std::vector<Pair>> lowrank_, deferred_;
+    std::map<std::pair<int, long long>, int64_t> coup_off_;
+    double *arena_ = nullptr, *skel_ = nullptr;
+    std::vector<double *> skel_diag_;
+    std::map<Pair, double *> skel_off_;
+
+    // per-wave state
+    int s_ = 0;
+    double *d_mu_ = nullptr, *d_tol_ = nullptr, *d_dropped_ = nullptr;
+    int64_t *d_counts_ = nullptr;
+    int *d_status_ = nullptr, *d_rank_ = nullptr;
+    std::vector<Cl> cl_;
+    std::vector<Blk> diag_;
+    std::vector<char> elim_;
+    std::map<Pair, Blk> offd_, coup_, fill_;
+    std::vector<std::set<Pair>> adj_off_, adj_fill_, adj_coup_;
+    h2l_stats *st_acc_ = nullptr;
+
+    // ---------------------------------------------------------------- helpers
+    static int node(int level, int i) { return (1 << level) - 1 + i; }
+    int csize(int level, int i) const {
+        const int nd = node(level, i);
+        return (int)(ranges_[2 * nd + 1] - ranges_[2 * nd]);
+    }
+    int lsize(int i) const { return csize(depth_, i); }
+    // arena pointer of the square leaf basis or nullptr when Q = I (rank 0)
+    const double *leaf_basis(int i) const {
+        const int nd = node(depth_, i);
+        if (boff_[nd] < 0 || brank_[nd] <= 0) return nullptr;
+        return arena_ + boff_[nd];
+    }
+
+    void free_payload() {
+        if (arena_) cudaFree(arena_);
+        if (skel_) cudaFree(skel_);
+        arena_ = skel_ = nullptr;
+        uploaded_ = false;
+    }
+
+    const void *stage(const void *src, size_t nbytes) {
+        const size_t bytes = (nbytes + 255) / 256 * 256;
+        if (stage_.off + bytes > stage_.cap) {
+            CK(cudaStreamSynchronize(st_));
+            stage_.off = 0;
+            if (bytes > stage_.cap) {
+                stage_.release();
+                stage_.init(bytes * 2);
+            }
+        }
+        char *h = stage_.h + stage_.off;
+        char *d = stage_.d + stage_.off;
+        std::memcpy(h, src, nbytes);
+        CK(cudaMemcpyAsync(d, h, nbytes, cudaMemcpyHostToDevice, st_));
+        stage_.off += bytes;
+        return d;
+    }
+    void sync() {
+        CK(cudaStreamSynchronize(st_));
+        stage_.off = 0;
+    }
+
+    Blk alloc(int rows, int cols, bool zero) {
+        Blk b;
+        b.rows = rows;
+        b.cols = cols;
+        b.bs = pad4((int64_t)rows * cols);
+        if (rows > 0 && cols > 0) {
+            CK(cudaMallocAsync((void **)&b.p, sizeof(double) * b.bs * s_, st_));
+            if (zero) CK(cudaMemsetAsync(b.p, 0, sizeof(double) * b.bs * s_, st_));
+        }
+        return b;
+    }
+    void release(Blk &b) {
+        if (b.p) CK(cudaFreeAsync(b.p, st_));
+        b = Blk{};
+    }
+
+    // -------------------------------------------------- batched task builders
+    struct CopyBatch {
+        std::vector<CopyTask> t;
+        std::vector<int> pre;
+        int tiles = 0;
+    };
+    struct GemmBatch {
+        std::vector<GemmTask> t;
+        std::vector<int> pre;
+        int tiles = 0;
+        double flops = 0;
+    };
+
+    static void add_copy(CopyBatch &b, const CopyTask &t) {
+        const int k = copy_tiles(t.rows, t.cols);
+        if (!k) return;
+        b.pre.push_back(b.tiles);
+        b.t.push_back(t);
+        b.tiles += k;
+    }
+    // dst <- op(src) (rows x cols) ; helpers
+    static CopyTask cp(const double *src, int64_t ss, int lds, double *dst, int64_t ds, int ldd,
+                       int rows, int cols, int trans = 0, int acc = 0, double alpha = 1.0) {
+        CopyTask t{};
+        t.src = src; t.dst = dst; t.sstride = ss; t.dstride = ds;
+        t.rows = rows; t.cols = cols; t.lds = lds; t.ldd = ldd;
+        t.trans = trans; t.acc = acc; t.alpha = alpha;
+        return t;
+    }
+    static CopyTask zero(double *dst, int64_t ds, int ldd, int rows, int cols) {
+        return cp(nullptr, 0, 0, dst, ds, ldd, rows, cols);
+    }
+    void flush(CopyBatch &b, const double *mu = nullptr) {
+        if (!b.t.empty()) {
+            const CopyTask *dt = (const CopyTask *)stage(b.t.data(), sizeof(CopyTask) * b.t.size());
+            const int *dp = (const int *)stage(b.pre.data(), sizeof(int) * b.pre.size());
+            launch_copy_prefixed(dt, dp, (int)b.t.size(), b.tiles, s_ ? s_ : 1, mu, st_);
+            CK(cudaGetLastError());
+            if (st_acc_) st_acc_->launches++;
+        }
+        b = CopyBatch{};
+    }
+    static void add_gemm(GemmBatch &b, const GemmTask &t, int nshift) {
+        const int k = gemm_tiles(t.M, t.N);
+        if (!k) return;
+        b.pre.push_back(b.tiles);
+        b.t.push_back(t);
+        b.tiles += k;
+        b.flops += 2.0 * t.M * t.N * (double)t.K * nshift;
+    }
+    static GemmTask gm(const double *A, int64_t sA, int lda, int tA, const double *B, int64_t sB,
+                       int ldb, int tB, double *C, int64_t sC, int ldc, int M, int N, int K,
+                       double alpha, double beta) {
+        GemmTask t{};
+        t.A = A; t.B = B; t.C = C; t.sA = sA; t.sB = sB; t.sC = sC;
+        t.M = M; t.N = N; t.K = K; t.lda = lda; t.ldb = ldb; t.ldc = ldc;
+        t.tA = tA; t.tB = tB; t.alpha = alpha; t.beta = beta;
+        return t;
+    }
+    cudaEvent_t next_event() {
+        if (ev_used_ == ev_pool_.size()) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            ev_pool_.push_back(e);
+        }
+        return ev_pool_[ev_used_++];
+    }
+    // kind: 1 = Schur update, 0 = other
+    void flush(GemmBatch &b, int nshift, int kind = 0) {
+        if (!b.t.empty()) {
+            const GemmTask *dt = (const GemmTask *)stage(b.t.data(), sizeof(GemmTask) * b.t.size());
+            const int *dp = (const int *)stage(b.pre.data(), sizeof(int) * b.pre.size());
+            const bool timed = time_kernels_ && kind == 1;
+            if (timed) CK(cudaEventRecord(mark(1), st_));
+            launch_gemm(dt, dp, (int)b.t.size(), b.tiles, nshift, st_);
+            CK(cudaGetLastError());
+            if (timed) CK(cudaEventRecord(next_event(), st_));
+            if (st_acc_) {
+                st_acc_->launches++;
+                st_acc_->flops += b.flops;
+                if (kind == 1) st_acc_->schur_flops += b.flops;
+            }
+        }
+        b = GemmBatch{};
+    }
+    cudaEvent_t mark(int kind) {
+        ev_marks_.push_back({(int)ev_used_, (double)kind});
+        return next_event();
+    }
+
+    // C (ra x cb) = Qa^T A Qb, Q == nullptr means identity (exact copy)
+    void congruence(const double *A, int ra, int cb, const double *Qa, const double *Qb,
+                    double *C, double *tmp) {
+        const int s_save = s_;
+        s_ = 1;
+        if (!Qa && !Qb) {
+            CopyBatch c;
+            add_copy(c, cp(A, 0, cb, C, 0, cb, ra, cb));
+            flush(c);
+        } else {
+            GemmBatch g;
+            const double *left = A;
+            if (Qa) {  // tmp = Qa^T A
+                add_gemm(g, gm(Qa, 0, ra, 1, A, 0, cb, 0, tmp, 0, cb, ra, cb, ra, 1.0, 0.0), 1);
+                flush(g, 1);
+                left = tmp;
+            }
+            if (Qb) {  // C = left Qb
+                add_gemm(g, gm(left, 0, cb, 0, Qb, 0, cb, 0, C, 0, cb, ra, cb, cb, 1.0, 0.0), 1);
+                flush(g, 1);
+            } else {
+                CopyBatch c;
+                add_copy(c, cp(left, 0, cb, C, 0, cb, ra, cb));
+                flush(c);
+            }
+        }
+        s_ = s_save;
+    }
+
+    Blk &pair_block(std::map<Pair, Blk> &store, int a, int b) { return store[{a, b}]; }
+
+    // ------------------------------------------------------------------ wave
+    void run_wave(const double *mu, int s, int64_t *counts, int32_t *status, h2l_stats &acc) {
+        s_ = s;
+        st_acc_ = &acc;
+        ev_used_ = 0;
+        ev_marks_.clear();
+        std::vector<double> tol(s);
+        for (int z = 0; z < s; ++z) tol[z] = eps_ * (scale0_ + std::fabs(mu[z]));
+        CK(cudaMallocAsync((void **)&d_mu_, sizeof(double) * s, st_));
+        CK(cudaMallocAsync((void **)&d_tol_, sizeof(double) * s, st_));
+        CK(cudaMallocAsync((void **)&d_dropped_, sizeof(double) * s, st_));
+        CK(cudaMallocAsync((void **)&d_counts_, sizeof(int64_t) * 3 * s, st_));
+        CK(cudaMallocAsync((void **)&d_status_, sizeof(int) * s, st_));
+        CK(cudaMallocAsync((void **)&d_rank_, sizeof(int) * s, st_));
+        CK(cudaMemcpyAsync(d_mu_, stage(mu, sizeof(double) * s), sizeof(double) * s,
+                           cudaMemcpyDeviceToDevice, st_));
+        CK(cudaMemcpyAsync(d_tol_, stage(tol.data(), sizeof(double) * s), sizeof(double) * s,
+                           cudaMemcpyDeviceToDevice, st_));
+        CK(cudaMemsetAsync(d_counts_, 0, sizeof(int64_t) * 3 * s, st_));
+        CK(cudaMemsetAsync(d_status_, 0, sizeof(int) * s, st_));
+
+        if (depth_ == 0) {
+            Blk root = alloc(lsize(0), lsize(0), false);
+            CopyBatch c;
+            CopyTask t = cp(skel_diag_[0], 0, root.cols, root.p, root.bs, root.cols, root.rows,
+                            root.cols);
+            t.shift_diag = 1;
+            add_copy(c, t);
+            flush(c, d_mu_);
+            factor_root(root);
+            release(root);
+        } else {
+            assemble_leaf();
+            int level = depth_;
+            Blk root;
+            while (true) {
+                process_level(level);
+                if (kind_ == H2L_FLAT) {
+                    root = merge_flat();
+                    break;
+                }
+                if (level == 1) {
+                    root = merge_pairwise(1, true);
+                    break;
+                }
+                merge_pairwise(level, false);
+                --level;
+            }
+            factor_root(root);
+            release(root);
+            clear_level();
+        }
+        // timings of Schur launches
+        std::vector<int64_t> hc(3 * s);
+        std::vector<int> hs(s);
+        std::vector<double> hd(s);
+        CK(cudaMemcpyAsync(hc.data(), d_counts_, sizeof(int64_t) * 3 * s, cudaMemcpyDeviceToHost, st_));
+        CK(cudaMemcpyAsync(hs.data(), d_status_, sizeof(int) * s, cudaMemcpyDeviceToHost, st_));
+        sync();
+        for (auto &mk : ev_marks_) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, ev_pool_[mk.first], ev_pool_[mk.first + 1]));
+            if (mk.second == 1) acc.ms_schur += ms;
+        }
+        std::memcpy(counts, hc.data(), sizeof(int64_t) * 3 * s);
+        for (int z = 0; z < s; ++z) status[z] = hs[z] ? H2L_SHIFT_SINGULAR : H2L_SHIFT_OK;
+        for (double *p : {d_mu_, d_tol_, d_dropped_}) CK(cudaFreeAsync(p, st_));
+        CK(cudaFreeAsync(d_counts_, st_));
+        CK(cudaFreeAsync(d_status_, st_));
+        CK(cudaFreeAsync(d_rank_, st_));
+        sync();
+        st_acc_ = nullptr;
+    }
+
+    void clear_level() {
+        for (auto &b : diag_) release(b);
+        for (auto &kv : offd_) release(kv.second);
+        for (auto &kv : coup_) release(kv.second);
+        for (auto &kv : fill_) release(kv.second);
+        diag_.clear();
+        offd_.clear();
+        coup_.clear();
+        fill_.clear();
+    }
+
+    void reset_adjacency(int nclus) {
+        adj_off_.assign(nclus, {});
+        adj_fill_.assign(nclus, {});
+        adj_coup_.assign(nclus, {});
+        elim_.assign(nclus, 0);
+    }
+
+    // load couplings of `level` from the arena into s-batched blocks
+    void load_couplings(int level, CopyBatch &c) {
+        auto it = lowrank_.find(level);
+        if (it == lowrank_.end()) return;
+        for (auto &pr : it->second) {
+            const int i = pr.first, j = pr.second;
+            const int ri = brank_[node(level, i)], rj = brank_[node(level, j)];
+            Blk b = alloc(ri, rj, false);
+            const int64_t off = coup_off_.at({level, i * 1000003LL + j});
+            if (b.p) add_copy(c, cp(arena_ + off, 0, rj, b.p, b.bs, rj, ri, rj));
+            coup_[pr] = b;
+            adj_coup_[i].insert(pr);
+            adj_coup_[j].insert(pr);
+        }
+    }
+
+    void assemble_leaf() {
+        const int L = depth_, nl = 1 << L;
+        clear_level();
+        cl_.assign(nl, Cl{});
+        diag_.assign(nl, Blk{});
+        reset_adjacency(nl);
+        CopyBatch c;
+        for (int i = 0; i < nl; ++i) {
+            const int m = lsize(i);
+            if (m == 0) continue;
+            const int r = std::max(0, brank_[node(L, i)]);
+            cl_[i] = Cl{m, m - r, r, r};
+            diag_[i] = alloc(m, m, false);
+            CopyTask t = cp(skel_diag_[i], 0, m, diag_[i].p, diag_[i].bs, m, m, m);
+            t.shift_diag = 1;
+            add_copy(c, t);
+        }
+        for (auto &pr : dense_) {
+            const int i = pr.first, j = pr.second;
+            Blk b = alloc(lsize(i), lsize(j), false);
+            add_copy(c, cp(skel_off_.at(pr), 0, b.cols, b.p, b.bs, b.cols, b.rows, b.cols));
+            offd_[pr] = b;
+            adj_off_[i].insert(pr);
+            adj_off_[j].insert(pr);
+        }
+        load_couplings(L, c);
+        flush(c, d_mu_);
+    }
+
+    void process_level(int level) {
+        const int nc = 1 << level;
+        for (int i = 0; i < nc; ++i) {
+            if (cl_[i].m == 0) continue;
+            recompress(i);
+            eliminate(i);
+        }
+        // fold fills of this level's low-rank pairs into the couplings (gldl.py:284-294)
+        auto it = lowrank_.find(level);
+        if (it != lowrank_.end()) {
+            CopyBatch c;
+            std::vector<Pair> done;
+            for (auto &pr : it->second) {
+                auto f = fill_.find(pr);
+                if (f == fill_.end()) continue;
+                Blk &C = coup_.at(pr);
+                Blk &F = f->second;
+                const int a = pr.first, b = pr.second;
+                const int ra = cl_[a].nR, rb = cl_[b].nR;
+                if (C.p)
+                    add_copy(c, cp(F.at(ra, rb), F.bs, F.cols, C.p, C.bs, C.cols, C.rows, C.cols, 0, 1));
+                done.push_back(pr);
+            }
+            flush(c);
+            for (auto &pr : done) {
+                release(fill_[pr]);
+                fill_.erase(pr);
+                adj_fill_[pr.first].erase(pr);
+                adj_fill_[pr.second].erase(pr);
+            }
+        }
+    }
+
+    // ------------------------------------------------------- recompression K7-K9
+    void row_transform(const Blk &src, Blk &dst, const double *Tr, int64_t trs, int nR, int nS,
+                       int t, GemmBatch &g, CopyBatch &c) {
+        // dst rows: [0,newR) = Tr[0:newR] src[0:nR]; [newR,newR+nS) = src[nR:]; [newR+nS,m) = Tr[newR:] src[0:nR]
+        const int newR = nR - t, cols = src.cols;
+        add_gemm(g, gm(Tr, trs, nR, 0, src.p, src.bs, cols, 0, dst.p, dst.bs, cols, newR, cols, nR,
+                       1.0, 0.0), s_);
+        add_gemm(g, gm(Tr + (int64_t)newR * nR, trs, nR, 0, src.p, src.bs, cols, 0,
+                       dst.at(newR + nS, 0), dst.bs, cols, t, cols, nR, 1.0, 0.0), s_);
+        add_copy(c, cp(src.at(nR, 0), src.bs, cols, dst.at(newR, 0), dst.bs, cols, nS, cols));
+    }
+    void col_transform(const Blk &src, Blk &dst, const double *Tr, int64_t trs, int nR, int nS,
+                       int t, GemmBatch &g, CopyBatch &c) {
+        // dst cols: [0,newR) = src[:,0:nR] Tr[0:newR]^T ; [newR,newR+nS) = src[:,nR:] ; rest = src[:,0:nR] Tr[newR:]^T
+        const int newR = nR - t, rows = src.rows, m = src.cols;
+        add_gemm(g, gm(src.p, src.bs, m, 0, Tr, trs, nR, 1, dst.p, dst.bs, m, rows, newR, nR, 1.0,
+                       0.0), s_);
+        add_gemm(g, gm(src.p, src.bs, m, 0, Tr + (int64_t)newR * nR, trs, nR, 1,
+                       dst.at(0, newR + nS), dst.bs, m, rows, t, nR, 1.0, 0.0), s_);
+        add_copy(c, cp(src.at(0, nR), src.bs, m, dst.at(0, newR), dst.bs, m, rows, nS));
+    }
+
+    void recompress(int i) {
+        Cl &ci = cl_[i];
+        const int nR = ci.nR;
+        auto &keys = adj_fill_[i];
+        if (nR == 0 || keys.empty()) return;
+        std::vector<Pair> ks(keys.begin(), keys.end());
+        int c = 0;
+        for (auto &k : ks) c += (k.first == i) ? fill_.at(k).cols : fill_.at(k).rows;
+        if (c > 0) {
+            // G^T (c x nR): row q = column q of G
+            Blk GT = alloc(c, nR, false);
+            CopyBatch cb;
+            int q0 = 0;
+            for (auto &k : ks) {
+                Blk &F = fill_.at(k);
+                if (k.first == i) {  // part = F[:nR, :]  -> GT rows = columns of F
+                    add_copy(cb, cp(F.p, F.bs, F.cols, GT.at(q0, 0), GT.bs, nR, F.cols, nR, 1));
+                    q0 += F.cols;
+                } else {  // part = F[:, :nR]^T -> GT rows = rows of F
+                    add_copy(cb, cp(F.p, F.bs, F.cols, GT.at(q0, 0), GT.bs, nR, F.rows, nR, 0));
+                    q0 += F.rows;
+                }
+            }
+            flush(cb);
+            const int64_t vs = pad4(nR), cs = pad4(c);
+            double *tau, *norms;
+            int *piv, *used;
+            CK(cudaMallocAsync((void **)&tau, sizeof(double) * vs * s_, st_));
+            CK(cudaMallocAsync((void **)&piv, sizeof(int) * vs * s_, st_));
+            CK(cudaMallocAsync((void **)&used, sizeof(int) * cs * s_, st_));
+            CK(cudaMallocAsync((void **)&norms, sizeof(double) * cs * s_, st_));
+            int *d_active;
+            CK(cudaMallocAsync((void **)&d_active, sizeof(int) * s_, st_));
+            activity_from_status(d_active);
+            CK(launch_pqr(GT.p, GT.bs, c, nR, nR, tau, piv, used, norms, vs, cs, d_tol_, d_rank_,
+                          d_dropped_, d_active, -1, s_, st_));
+            st_acc_->launches += 2;
+            std::vector<int> rk(s_), act(s_);
+            std::vector<double> dr(s_);
+            CK(cudaMemcpyAsync(rk.data(), d_rank_, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
+            CK(cudaMemcpyAsync(act.data(), d_active, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
+            CK(cudaMemcpyAsync(dr.data(), d_dropped_, sizeof(double) * s_, cudaMemcpyDeviceToHost, st_));
+            sync();
+            int t = 0;
+            for (int z = 0; z < s_; ++z)
+                if (act[z]) {
+                    t = std::max(t, rk[z]);
+                    st_acc_->dropped_fro += dr[z];
+                }
+            st_acc_->recompressions++;
+            st_acc_->flops += 4.0 * c * nR * (double)std::max(t, 1) * s_;
+            if (t > 0) {
+                CK(launch_pqr(GT.p, GT.bs, c, nR, nR, tau, piv, used, norms, vs, cs, d_tol_, d_rank_,
+                              d_dropped_, d_active, t, s_, st_));
+                Blk Tr = alloc(nR, nR, false);
+                CK(launch_form_tr(GT.p, GT.bs, nR, tau, piv, vs, nR, t, Tr.p, Tr.bs, d_active, s_, st_));
+                st_acc_->launches += 2;
+                apply_rotation(i, Tr, t);
+                release(Tr);
+                ci.nR = nR - t;
+                ci.nS += t;
+                st_acc_->rank_added += t;
+            }
+            CK(cudaFreeAsync(tau, st_));
+            CK(cudaFreeAsync(piv, st_));
+            CK(cudaFreeAsync(used, st_));
+            CK(cudaFreeAsync(norms, st_));
+            CK(cudaFreeAsync(d_active, st_));
+            release(GT);
+        }
+        // discard what is left in the redundant rows of i's fills (gldl.py:341-347)
+        CopyBatch z;
+        const int keep = ci.nR;
+        for (auto &k : ks) {
+            Blk &F = fill_.at(k);
+            if (keep == 0) continue;
+            if (k.first == i) add_copy(z, zero(F.p, F.bs, F.cols, keep, F.cols));
+            else add_copy(z, zero(F.p, F.bs, F.cols, F.rows, keep));
+        }
+        flush(z);
+    }
+
+    void activity_from_status(int *d_active);
+
+    void apply_rotation(int i, const Blk &Tr, int t) {
+        Cl &ci = cl_[i];
+        const int nR = ci.nR, nS = ci.nS, m = ci.m;
+        GemmBatch g1, g2;
+        CopyBatch c1, c2;
+        // diag: Y = T D ; Z = Y T^T
+        Blk Y = alloc(m, m, false), Z = alloc(m, m, false);
+        row_transform(diag_[i], Y, Tr.p, Tr.bs, nR, nS, t, g1, c1);
+        std::vector<std::pair<Blk *, Blk>> repl;
+        for (auto *store : {&offd_, &fill_}) {
+            auto &adj = (store == &offd_) ? adj_off_[i] : adj_fill_[i];
+            for (auto &k : adj) {
+                Blk &B = store->at(k);
+                Blk N = alloc(B.rows, B.cols, false);
+                if (k.first == i) row_transform(B, N, Tr.p, Tr.bs, nR, nS, t, g1, c1);
+                else col_transform(B, N, Tr.p, Tr.bs, nR, nS, t, g1, c1);
+                repl.push_back({&B, N});
+            }
+        }
+        flush(g1, s_);
+        flush(c1);
+        col_transform(Y, Z, Tr.p, Tr.bs, nR, nS, t, g2, c2);
+        // couplings: zero-pad by t rows/cols (gldl.py:324-330)
+        std::vector<std::pair<Blk *, Blk>> crepl;
+        for (auto &k : adj_coup_[i]) {
+            Blk &C = coup_.at(k);
+            Blk N = (k.first == i) ? alloc(C.rows + t, C.cols, true) : alloc(C.rows, C.cols + t, true);
+            if (C.p && N.p) add_copy(c2, cp(C.p, C.bs, C.cols, N.p, N.bs, N.cols, C.rows, C.cols));
+            crepl.push_back({&C, N});
+        }
+        flush(g2, s_);
+        flush(c2);
+        release(diag_[i]);
+        release(Y);
+        diag_[i] = Z;
+        for (auto &r : repl) { release(*r.first); *r.first = r.second; }
+        for (auto &r : crepl) { release(*r.first); *r.first = r.second; }
+    }
+
+    // --------------------------------------------------------- elimination K2-K6
+    void eliminate(int i) {
+        Cl &ci = cl_[i];
+        const int nR = ci.nR, nS = ci.nS, m = ci.m;
+        if (nR == 0) return;
+        st_acc_->max_front = std::max<int64_t>(st_acc_->max_front, m);
+        Blk &D = diag_[i];
+        // ---- K2/K3: BK of D[:nR,:nR] with fused inertia
+        const int64_t ps = pad4(nR);
+        int *perm;
+        double *dinfo;
+        CK(cudaMallocAsync((void **)&perm, sizeof(int) * ps * s_, st_));
+        CK(cudaMallocAsync((void **)&dinfo, sizeof(double) * 3 * ps * s_, st_));
+        bk_launch(D.p, D.bs, m, nR, perm, dinfo, ps);
+        // ---- partners and live rows
+        std::vector<int> partners;
+        for (auto &k : adj_off_[i]) partners.push_back(k.first == i ? k.second : k.first);
+        std::sort(partners.begin(), partners.end());
+        struct Seg { int who, lo, len, row; };
+        std::vector<Seg> segs;
+        int R = 0;
+        segs.push_back({i, nR, nS, 0});
+        R += nS;
+        for (int j : partners) {
+            const int lo = elim_[j] ? cl_[j].nR : 0;
+            segs.push_back({j, lo, cl_[j].m - lo, R});
+            R += cl_[j].m - lo;
+        }
+        double flops = (double)nR * nR * nR / 3.0 + (double)R * nR * nR + (double)R * nR;
+        if (R > 0) {
+            // ---- K4/K5: panel W = B P^T L^{-T}, X = W D^{-1}
+            Blk Wb = alloc(R, nR, false), Xb = alloc(R, nR, false);
+            std::vector<PanelTile> tiles;
+            for (auto &sg : segs) {
+                if (sg.len <= 0) continue;
+                const double *src;
+                int lds, trans, r0;
+                if (sg.who == i) {  // D[nR:, :nR]
+                    src = D.at(nR, 0); lds = m; trans = 0; r0 = 0;
+                } else {
+                    const int j = sg.who;
+                    if (i < j) {  // offd(i,j)[:nR, :]^T
+                        Blk &O = offd_.at({i, j});
+                        src = O.p; lds = O.cols; trans = 1; r0 = sg.lo;
+                    } else {      // offd(j,i)[:, :nR]
+                        Blk &O = offd_.at({j, i});
+                        src = O.p; lds = O.cols; trans = 0; r0 = sg.lo;
+                    }
+                }
+                const int64_t ss = (sg.who == i) ? D.bs
+                                   : (i < sg.who ? offd_.at({i, sg.who}).bs : offd_.at({sg.who, i}).bs);
+                for (int r = 0; r < sg.len; r += PANEL_ROWS) {
+                    PanelTile t{};
+                    t.src = src; t.sstride = ss; t.lds = lds; t.trans = trans;
+                    t.row0 = sg.row + r; t.nrows = std::min(PANEL_ROWS, sg.len - r);
+                    t.src_row0 = r0 + r;
+                    tiles.push_back(t);
+                }
+            }
+            const PanelTile *dt = (const PanelTile *)stage(tiles.data(), sizeof(PanelTile) * tiles.size());
+            CK(launch_panel(dt, (int)tiles.size(), s_, D.p, D.bs, m, nR, perm, dinfo, ps, Wb.p, Xb.p,
+                            Wb.bs, nR, st_));
+            st_acc_->launches++;
+            // ---- K6: Schur updates of every target pair, one grouped launch
+            GemmBatch g;
+            double sch = 0.0;
+            auto upd = [&](const Seg &a, const Seg &b, double *C, int64_t sC, int ldc) {
+                if (a.len <= 0 || b.len <= 0) return;
+                add_gemm(g, gm(Xb.at(a.row, 0), Xb.bs, nR, 0, Wb.at(b.row, 0), Wb.bs, nR, 1, C, sC,
+                               ldc, a.len, b.len, nR, -1.0, 1.0), s_);
+                sch += (a.who == b.who ? 1.0 : 2.0) * (double)a.len * b.len * nR;
+            };
+            upd(segs[0], segs[0], D.at(nR, nR), D.bs, m);
+            for (size_t x = 1; x < segs.size(); ++x) {
+                const Seg &sj = segs[x];
+                const int j = sj.who;
+                Blk &Dj = diag_[j];
+                upd(sj, sj, Dj.at(sj.lo, sj.lo), Dj.bs, Dj.cols);
+                if (i < j) {
+                    Blk &O = offd_.at({i, j});
+                    upd(segs[0], sj, O.at(nR, sj.lo), O.bs, O.cols);
+                } else {
+                    Blk &O = offd_.at({j, i});
+                    upd(sj, segs[0], O.at(sj.lo, nR), O.bs, O.cols);
+                }
+            }
+            for (size_t x = 1; x < segs.size(); ++x)
+                for (size_t y = x + 1; y < segs.size(); ++y) {
+                    const Seg &a = segs[x], &b = segs[y];
+                    const Pair key{a.who, b.who};
+                    Blk *T;
+                    auto o = offd_.find(key);
+                    if (o != offd_.end()) {
+                        T = &o->second;
+                    } else {
+                        auto f = fill_.find(key);
+                        if (f == fill_.end()) {
+                            fill_[key] = alloc(cl_[a.who].m, cl_[b.who].m, true);
+                            adj_fill_[a.who].insert(key);
+                            adj_fill_[b.who].insert(key);
+                            st_acc_->fill_blocks++;
+                            f = fill_.find(key);
+                        }
+                        T = &f->second;
+                    }
+                    upd(a, b, T->at(a.lo, b.lo), T->bs, T->cols);
+                }
+            flops += sch;
+            flush(g, s_, 1);
+            release(Wb);
+            release(Xb);
+        }
+        st_acc_->flops += flops * s_;
+        // ---- retire the redundant rows / columns of i (gldl.py:411-417)
+        CopyBatch zc;
+        add_copy(zc, zero(D.p, D.bs, m, nR, m));
+        add_copy(zc, zero(D.at(nR, 0), D.bs, m, m - nR, nR));
+        for (auto &k : adj_off_[i]) {
+            Blk &O = offd_.at(k);
+            if (k.first == i) add_copy(zc, zero(O.p, O.bs, O.cols, nR, O.cols));
+            else add_copy(zc, zero(O.p, O.bs, O.cols, O.rows, nR));
+        }
+        flush(zc);
+        CK(cudaFreeAsync(perm, st_));
+        CK(cudaFreeAsync(dinfo, st_));
+        elim_[i] = 1;
+    }
+
+    void bk_launch(double *a, int64_t astride, int ld, int n, int *perm, double *dinfo, int64_t ps) {
+        BkJob jb{a, astride, ld, n, perm, dinfo, ps};
+        const BkJob *dj = (const BkJob *)stage(&jb, sizeof(jb));
+        const int64_t scr = bk_scratch_doubles(n);
+        double *scratch = nullptr;
+        if (scr) CK(cudaMallocAsync((void **)&scratch, sizeof(double) * scr * s_, st_));
+        CK(launch_bk_engine(dj, 1, s_, n, d_counts_, d_status_, scratch, scr, st_));
+        st_acc_->launches++;
+        if (scratch) CK(cudaFreeAsync(scratch, st_));
+    }
+
+    void factor_root(Blk &root) {
+        if (root.rows == 0 || !root.p) return;
+        const int n = root.rows;
+        const int64_t ps = pad4(n);
+        int *perm;
+        double *dinfo;
+        CK(cudaMallocAsync((void **)&perm, sizeof(int) * ps * s_, st_));
+        CK(cudaMallocAsync((void **)&dinfo, sizeof(double) * 3 * ps * s_, st_));
+        bk_launch(root.p, root.bs, root.cols, n, perm, dinfo, ps);
+        st_acc_->flops += (double)n * n * n / 3.0 * s_;
+        CK(cudaFreeAsync(perm, st_));
+        CK(cudaFreeAsync(dinfo, st_));
+    }
+
+    // ----------------------------------------------------------------- merges
+    // skeleton-skeleton content of a finished pair (gldl.py:429-438)
+    bool content(const Pair &k, const double **p, int64_t *bs, int *ld, int *rows, int *cols) {
+        auto c = coup_.find(k);
+        if (c != coup_.end()) {
+            *p = c->second.p; *bs = c->second.bs; *ld = c->second.cols;
+            *rows = c->second.rows; *cols = c->second.cols;
+            return c->second.p != nullptr;
+        }
+        const Blk *B = nullptr;
+        auto o = offd_.find(k);
+        if (o != offd_.end()) B = &o->second;
+        else {
+            auto f = fill_.find(k);
+            if (f != fill_.end()) B = &f->second;
+        }
+        if (!B || !B->p) return false;
+        const int ra = cl_[k.first].nR, rb = cl_[k.second].nR;
+        *p = B->at(ra, rb); *bs = B->bs; *ld = B->cols;
+        *rows = B->rows - ra; *cols = B->cols - rb;
+        return *rows > 0 && *cols > 0;
+    }
+
+    std::set<Pair> all_pairs() const {
+        std::set<Pair> u;
+        for (auto &kv : coup_) u.insert(kv.first);
+        for (auto &kv : offd_) u.insert(kv.first);
+        for (auto &kv : fill_) u.insert(kv.first);
+        return u;
+    }
+
+    Blk merge_flat() {
+        const int nl = 1 << depth_;
+        std::vector<int> start(nl);
+        int tot = 0;
+        for (int i = 0; i < nl; ++i) { start[i] = tot; tot += cl_[i].nS; }
+        Blk R = alloc(tot, tot, true);
+        CopyBatch c;
+        for (int i = 0; i < nl; ++i) {
+            const Cl &ci = cl_[i];
+            if (ci.nS == 0 || !diag_[i].p) continue;
+            add_copy(c, cp(diag_[i].at(ci.nR, ci.nR), diag_[i].bs, ci.m, R.at(start[i], start[i]),
+                           R.bs, tot, ci.nS, ci.nS));
+        }
+        for (auto &k : all_pairs()) {
+            const double *p; int64_t bs; int ld, rows, cols;
+            if (!content(k, &p, &bs, &ld, &rows, &cols)) continue;
+            add_copy(c, cp(p, bs, ld, R.at(start[k.first], start[k.second]), R.bs, tot, rows, cols));
+            add_copy(c, cp(p, bs, ld, R.at(start[k.second], start[k.first]), R.bs, tot, cols, rows, 1));
+        }
+        flush(c);
+        return R;
+    }
+
+    Blk merge_pairwise(int level, bool to_root) {
+        const int np = 1 << (level - 1);
+        std::vector<int> loc(2 * np), msz(np);
+        for (int p = 0; p < np; ++p) {
+            loc[2 * p] = 0;
+            loc[2 * p + 1] = cl_[2 * p].nS;
+            msz[p] = cl_[2 * p].nS + cl_[2 * p + 1].nS;
+        }
+        std::vector<Blk> raw(np);
+        CopyBatch c;
+        for (int p = 0; p < np; ++p) {
+            const int c1 = 2 * p, c2 = 2 * p + 1;
+            const int s1 = cl_[c1].nS, s2 = cl_[c2].nS;
+            raw[p] = alloc(s1 + s2, s1 + s2, true);
+            if (!raw[p].p) continue;
+            const int mp = s1 + s2;
+            if (s1) add_copy(c, cp(diag_[c1].at(cl_[c1].nR, cl_[c1].nR), diag_[c1].bs, cl_[c1].m,
+                                   raw[p].p, raw[p].bs, mp, s1, s1));
+            if (s2) add_copy(c, cp(diag_[c2].at(cl_[c2].nR, cl_[c2].nR), diag_[c2].bs, cl_[c2].m,
+                                   raw[p].at(s1, s1), raw[p].bs, mp, s2, s2));
+            const double *q; int64_t bs; int ld, rows, cols;
+            if (content({c1, c2}, &q, &bs, &ld, &rows, &cols)) {
+                add_copy(c, cp(q, bs, ld, raw[p].at(0, s1), raw[p].bs, mp, rows, cols));
+                add_copy(c, cp(q, bs, ld, raw[p].at(s1, 0), raw[p].bs, mp, cols, rows, 1));
+            }
+        }
+        std::map<Pair, Blk> rawpair;
+        for (auto &k : all_pairs()) {
+            const int p = k.first >> 1, q = k.second >> 1;
+            if (p == q) continue;
+            const double *src; int64_t bs; int ld, rows, cols;
+            if (!content(k, &src, &bs, &ld, &rows, &cols)) continue;
+            auto it = rawpair.find({p, q});
+            if (it == rawpair.end()) it = rawpair.emplace(Pair{p, q}, alloc(msz[p], msz[q], true)).first;
+            Blk &dst = it->second;
+            add_copy(c, cp(src, bs, ld, dst.at(loc[k.first], loc[k.second]), dst.bs, dst.cols, rows, cols));
+        }
+        flush(c);
+        if (to_root) {
+            for (auto &kv : rawpair) release(kv.second);
+            for (int p = 1; p < np; ++p) release(raw[p]);
+            return raw[0];
+        }
+        const int pl = level - 1;
+        // parent bases (shift independent): [U_R | extras | U_S] (gldl.py:561-588)
+        std::vector<Cl> ncl(np);
+        std::vector<const double *> Q(np, nullptr);
+        std::vector<double *> Qown;
+        CopyBatch qc;
+        for (int p = 0; p < np; ++p) {
+            const int mp = msz[p];
+            if (mp == 0) continue;
+            const Cl &a = cl_[2 * p], &b = cl_[2 * p + 1];
+            const int nd = node(pl, p);
+            const int rk = std::max(0, brank_[nd]);
+            const int e1 = a.nS - a.r0, e2 = b.nS - b.r0;
+            const double *bq = boff_[nd] >= 0 ? arena_ + boff_[nd] : nullptr;
+            const int m0 = bdim_[nd];
+            ncl[p] = Cl{mp, mp - rk, rk, rk};
+            if (e1 == 0 && e2 == 0) {
+                Q[p] = bq;  // arena square basis, m0 == mp
+                continue;
+            }
+            double *qp;
+            CK(cudaMallocAsync((void **)&qp, sizeof(double) * (int64_t)mp * mp, st_));
+            CK(cudaMemsetAsync(qp, 0, sizeof(double) * (int64_t)mp * mp, st_));
+            Qown.push_back(qp);
+            Q[p] = qp;
+            const int nRh = a.r0 + b.r0 - rk;
+            // rows of the stored basis: [0, r0a) -> [0, r0a) ; [r0a, m0) -> [nSa, nSa + r0b)
+            if (bq && nRh > 0) {
+                add_copy(qc, cp(bq, 0, m0, qp, 0, mp, a.r0, nRh));
+                add_copy(qc, cp(bq + (int64_t)a.r0 * m0, 0, m0, qp + (int64_t)a.nS * mp, 0, mp, b.r0, nRh));
+            }
+            if (bq && rk > 0) {
+                add_copy(qc, cp(bq + (m0 - rk), 0, m0, qp + (mp - rk), 0, mp, a.r0, rk));
+                add_copy(qc, cp(bq + (int64_t)a.r0 * m0 + (m0 - rk), 0, m0,
+                                qp + (int64_t)a.nS * mp + (mp - rk), 0, mp, b.r0, rk));
+            }
+            if (e1 > 0) {
+                CopyTask t = zero(qp + (int64_t)a.r0 * mp + nRh, 0, mp, e1, e1);
+                t.ident = 1;
+                add_copy(qc, t);
+            }
+            if (e2 > 0) {
+                CopyTask t = zero(qp + (int64_t)(a.nS + b.r0) * mp + nRh + e1, 0, mp, e2, e2);
+                t.ident = 1;
+                add_copy(qc, t);
+            }
+        }
+        {   // Q construction uses a single shift
+            const int s_save = s_;
+            s_ = 1;
+            flush(qc);
+            s_ = s_save;
+        }
+        // new blocks: ndiag = Q^T raw Q ; offd/fill = Qp^T raw Qq
+        std::vector<Blk> ndiag(np);
+        std::map<Pair, Blk> noffd, nfill;
+        std::vector<Blk> tmps;
+        GemmBatch g1, g2;
+        auto congr = [&](const Blk &in, int p, int q, Blk &out) {
+            const int mp = msz[p], mq = msz[q];
+            out = alloc(mp, mq, false);
+            if (!out.p) return;
+            Blk tmp = alloc(mp, mq, false);
+            add_gemm(g1, gm(Q[p], 0, mp, 1, in.p, in.bs, mq, 0, tmp.p, tmp.bs, mq, mp, mq, mp, 1.0,
+                            0.0), s_);
+            add_gemm(g2, gm(tmp.p, tmp.bs, mq, 0, Q[q], 0, mq, 0, out.p, out.bs, mq, mp, mq, mq, 1.0,
+                            0.0), s_);
+            tmps.push_back(tmp);
+        };
+        for (int p = 0; p < np; ++p)
+            if (msz[p]) congr(raw[p], p, p, ndiag[p]);
+        std::vector<Blk> zeros;
+        auto dit = deferred_.find(pl);
+        if (dit != deferred_.end())
+            for (auto &k : dit->second) {
+                auto r = rawpair.find(k);
+                Blk in;
+                if (r != rawpair.end()) {
+                    in = r->second;
+                    rawpair.erase(r);
+                } else {
+                    in = alloc(msz[k.first], msz[k.second], true);
+                }
+                zeros.push_back(in);
+                congr(in, k.first, k.second, noffd[k]);
+            }
+        for (auto &kv : rawpair) {
+            congr(kv.second, kv.first.first, kv.first.second, nfill[kv.first]);
+            st_acc_->fill_blocks++;
+            zeros.push_back(kv.second);
+        }
+        flush(g1, s_);
+        flush(g2, s_);
+        for (auto &b : tmps) release(b);
+        for (auto &b : zeros) release(b);
+        for (auto &b : raw) release(b);
+        for (double *q : Qown) CK(cudaFreeAsync(q, st_));
+        // swap in the parent level
+        clear_level();
+        cl_ = ncl;
+        diag_ = ndiag;
+        reset_adjacency(np);
+        for (auto &kv : noffd) {
+            offd_[kv.first] = kv.second;
+            adj_off_[kv.first.first].insert(kv.first);
+            adj_off_[kv.first.second].insert(kv.first);
+        }
+        for (auto &kv : nfill) {
+            fill_[kv.first] = kv.second;
+            adj_fill_[kv.first.first].insert(kv.first);
+            adj_fill_[kv.first.second].insert(kv.first);
+        }
+        CopyBatch cc;
+        load_couplings(pl, cc);
+        flush(cc);
+        return Blk{};
+    }
+};
+
+}  // namespace h2l
+
+// ---------------------------------------------------------------- status glue
+namespace h2l {
+__global__ void active_kernel(const int *status, int *active, int s) {
+    int z = blockIdx.x * blockDim.x + threadIdx.x;
+    if (z < s) active[z] = status[z] == 0;
+}
+void Engine::activity_from_status(int *d_active) {
+    active_kernel<<<(s_ + 127) / 128, 128, 0, st_>>>(d_status_, d_active, s_);
+    CK(cudaGetLastError());
+}
+}  // namespace h2l
+
+// =================================================================== C ABI
+struct h2l_engine {
+    h2l::Engine *impl = nullptr;
+    std::string err;
+};
+
+static thread_local std::string g_err;
+
+template <class F>
+static int guarded(h2l_engine *e, F &&f) {
+    try {
+        f();
+        return H2L_OK;
+    } catch (const h2l::CudaFail &x) {
+        (e ? e->err : g_err) = x.what();
+        return x.code;
+    } catch (const std::bad_alloc &) {
+        (e ? e->err : g_err) = "host allocation failed";
+        return H2L_ENOMEM;
+    } catch (const std::exception &x) {
+        (e ? e->err : g_err) = x.what();
+        return H2L_EINVAL;
+    }
+}
+
+static int check_device(int device) {
+    int cnt = 0;
+    if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt <= 0) {
+        cudaGetLastError();
+        g_err = "no CUDA device";
+        return H2L_ENODEV;
+    }
+    if (device < 0 || device >= cnt) {
+        g_err = "device index out of range";
+        return H2L_ENODEV;
+    }
+    return H2L_OK;
+}
+
+extern "C" {
+
+int h2l_create(h2l_engine **engine, int device) {
+    if (!engine) return H2L_EINVAL;
+    *engine = nullptr;
+    int rc = check_device(device);
+    if (rc) return rc;
+    return guarded(nullptr, [&] {
+        auto *e = new h2l_engine;
+        try {
+            e->impl = new h2l::Engine(device);
+        } catch (...) {
+            delete e;
+            throw;
+        }
+        *engine = e;
+    });
+}
+
+int h2l_destroy(h2l_engine *engine) {
+    if (!engine) return H2L_OK;
+    delete engine->impl;
+    delete engine;
+    return H2L_OK;
+}
+
+const char *h2l_last_error(const h2l_engine *engine) {
+    return engine ? engine->err.c_str() : g_err.c_str();
+}
+
+int h2l_upload(h2l_engine *engine, const h2l_plan *plan) {
+    if (!engine || !plan) return H2L_EINVAL;
+    return guarded(engine, [&] { engine->impl->upload(plan); });
+}
+
+int h2l_inertia(h2l_engine *engine, const double *mu, int32_t s, int64_t *counts, int32_t *status,
+                h2l_stats *stats) {
+    if (!engine || (s > 0 && (!mu || !counts || !status)) || s < 0) return H2L_EINVAL;
+    if (s == 0) return H2L_OK;
+    return guarded(engine, [&] { engine->impl->inertia(mu, s, counts, status, stats); });
+}
+
+int h2l_set_option(h2l_engine *engine, const char *key, int64_t value) {
+    if (!engine || !key) return H2L_EINVAL;
+    return guarded(engine, [&] { engine->impl->set_option(key, value); });
+}
+
+int h2l_bk_factor(int device, double *a, int64_t n, int32_t count, int64_t *ipiv,
+                  const double *tol, int64_t *info) {
+    if (n < 0 || count < 0 || (count && (!a || !ipiv || !tol || !info))) return H2L_EINVAL;
+    if (n == 0 || count == 0) return H2L_OK;
+    int rc = check_device(device);
+    if (rc) return rc;
+    return guarded(nullptr, [&] {
+        CK(cudaSetDevice(device));
+        const size_t bytes = sizeof(double) * (size_t)n * n * count;
+        double *da, *dt, *ds = nullptr;
+        int64_t *dp, *di;
+        CK(cudaMalloc(&da, bytes));
+        CK(cudaMalloc(&dt, sizeof(double) * count));
+        CK(cudaMalloc(&dp, sizeof(int64_t) * n * count));
+        CK(cudaMalloc(&di, sizeof(int64_t) * count));
+        const int64_t scr = h2l::bk_scratch_doubles((int)n);
+        if (scr) CK(cudaMalloc(&ds, sizeof(double) * (size_t)n * (n + 1) / 2 * count));
+        CK(cudaMemcpy(da, a, bytes, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dt, tol, sizeof(double) * count, cudaMemcpyHostToDevice));
+        CK(cudaMemset(dp, 0, sizeof(int64_t) * n * count));
+        CK(h2l::launch_bk_kat(da, (int)n, count, dt, dp, di, ds, 0));
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpy(a, da, bytes, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(ipiv, dp, sizeof(int64_t) * n * count, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(info, di, sizeof(int64_t) * count, cudaMemcpyDeviceToHost));
+        cudaFree(da); cudaFree(dt); cudaFree(dp); cudaFree(di);
+        if (ds) cudaFree(ds);
+    });
+}
+
+int h2l_bk_inertia(int device, const double *a, int64_t n, int32_t count, const int64_t *ipiv,
+                   const double *zero_tol, int64_t *counts) {
+    if (n < 0 || count < 0 || (count && (!a || !ipiv || !zero_tol || !counts))) return H2L_EINVAL;
+    if (count == 0) return H2L_OK;
+    if (n == 0) {
+        std::memset(counts, 0, sizeof(int64_t) * 3 * count);
+        return H2L_OK;
+    }
+    int rc = check_device(device);
+    if (rc) return rc;
+    return guarded(nullptr, [&] {
+        CK(cudaSetDevice(device));
+        const size_t bytes = sizeof(double) * (size_t)n * n * count;
+        double *da, *dz;
+        int64_t *dp, *dc;
+        CK(cudaMalloc(&da, bytes));
+        CK(cudaMalloc(&dz, sizeof(double) * count));
+        CK(cudaMalloc(&dp, sizeof(int64_t) * n * count));
+        CK(cudaMalloc(&dc, sizeof(int64_t) * 3 * count));
+        CK(cudaMemcpy(da, a, bytes, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dz, zero_tol, sizeof(double) * count, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dp, ipiv, sizeof(int64_t) * n * count, cudaMemcpyHostToDevice));
+        CK(h2l::launch_bk_inertia(da, (int)n, count, dp, dz, dc, 0));
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpy(counts, dc, sizeof(int64_t) * 3 * count, cudaMemcpyDeviceToHost));
+        cudaFree(da); cudaFree(dz); cudaFree(dp); cudaFree(dc);
+    });
+}
+
+const char *h2l_version(void) { return "h2ldl 0.1 sm_100a"; }
+
+}  // extern "C"
