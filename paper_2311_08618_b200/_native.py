@@ -22,6 +22,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libh2ldl.so")
 
 H2L_OK = 0
+H2L_SHIFT_OK = 0
 H2L_SHIFT_SINGULAR = 1
 KIND = {"strong": 0, "weak": 1, "flat": 2}
 
