@@ -738,6 +738,24 @@ private:
     }
 
     // --------------------------------------------------------- elimination K2-K6
+    // one row segment of the elimination panel B = [D_SR ; partner slices]
+    struct Seg {
+        int who, lo, len, row;   // cluster, first live row, live rows, first panel row
+        const double *src;       // source block (shift 0)
+        int64_t ss;              // shift stride of the source
+        int lds, trans, r0;      // panel row r = src row (r0 + r), or column when trans
+    };
+    // op(segment) as the left operand (len x nR) of a GEMM
+    static void seg_as_A(const Seg &g, const double **A, int *lda, int *tA) {
+        if (g.trans) { *A = g.src + g.r0; *lda = g.lds; *tA = 1; }
+        else { *A = g.src + (int64_t)g.r0 * g.lds; *lda = g.lds; *tA = 0; }
+    }
+    // op(segment)^T as the right operand (nR x len) of a GEMM
+    static void seg_as_Bt(const Seg &g, const double **B, int *ldb, int *tB) {
+        if (g.trans) { *B = g.src + g.r0; *ldb = g.lds; *tB = 0; }
+        else { *B = g.src + (int64_t)g.r0 * g.lds; *ldb = g.lds; *tB = 1; }
+    }
+
     void eliminate(int i) {
         Cl &ci = cl_[i];
         const int nR = ci.nR, nS = ci.nS, m = ci.m;
@@ -751,62 +769,69 @@ private:
         CK(cudaMallocAsync((void **)&perm, sizeof(int) * ps * s_, st_));
         CK(cudaMallocAsync((void **)&dinfo, sizeof(double) * 3 * ps * s_, st_));
         bk_launch(D.p, D.bs, m, nR, perm, dinfo, ps);
-        // ---- partners and live rows
+        // ---- panel segments (live rows only)
         std::vector<int> partners;
         for (auto &k : adj_off_[i]) partners.push_back(k.first == i ? k.second : k.first);
         std::sort(partners.begin(), partners.end());
-        struct Seg { int who, lo, len, row; };
         std::vector<Seg> segs;
         int R = 0;
-        segs.push_back({i, nR, nS, 0});
+        segs.push_back({i, nR, nS, 0, D.at(nR, 0), D.bs, m, 0, 0});
         R += nS;
         for (int j : partners) {
             const int lo = elim_[j] ? cl_[j].nR : 0;
-            segs.push_back({j, lo, cl_[j].m - lo, R});
-            R += cl_[j].m - lo;
+            Seg g{j, lo, cl_[j].m - lo, R, nullptr, 0, 0, 0, lo};
+            if (i < j) {  // offd(i,j)[:nR, :]^T : panel rows = columns of the block
+                Blk &O = offd_.at({i, j});
+                g.src = O.p; g.ss = O.bs; g.lds = O.cols; g.trans = 1;
+            } else {      // offd(j,i)[:, :nR]
+                Blk &O = offd_.at({j, i});
+                g.src = O.p; g.ss = O.bs; g.lds = O.cols; g.trans = 0;
+            }
+            segs.push_back(g);
+            R += g.len;
         }
-        double flops = (double)nR * nR * nR / 3.0 + (double)R * nR * nR + (double)R * nR;
+        double flops = (double)nR * nR * nR / 3.0;
         if (R > 0) {
-            // ---- K4/K5: panel W = B P^T L^{-T}, X = W D^{-1}
-            Blk Wb = alloc(R, nR, false), Xb = alloc(R, nR, false);
+            // ---- K4/K5 as GEMMs.  The reference forms W = B P^T L^{-T} (dtrsm) and
+            // X = W D^{-1} (dgesv), then updates with X W^T.  Here the panel kernel
+            // solves the n x n identity once: W_I = P^T L^{-T}, X_I = W_I D^{-1}; then
+            // G = X_I W_I^T = P^T L^{-T} D^{-1} L^{-1} P, X = B G on the tensor pipe and
+            // the Schur update is X_a B_b^T (W = B is read in place from its blocks).
+            Blk WI = alloc(nR, nR, false), XI = alloc(nR, nR, false), G = alloc(nR, nR, false);
             std::vector<PanelTile> tiles;
-            for (auto &sg : segs) {
-                if (sg.len <= 0) continue;
-                const double *src;
-                int lds, trans, r0;
-                if (sg.who == i) {  // D[nR:, :nR]
-                    src = D.at(nR, 0); lds = m; trans = 0; r0 = 0;
-                } else {
-                    const int j = sg.who;
-                    if (i < j) {  // offd(i,j)[:nR, :]^T
-                        Blk &O = offd_.at({i, j});
-                        src = O.p; lds = O.cols; trans = 1; r0 = sg.lo;
-                    } else {      // offd(j,i)[:, :nR]
-                        Blk &O = offd_.at({j, i});
-                        src = O.p; lds = O.cols; trans = 0; r0 = sg.lo;
-                    }
-                }
-                const int64_t ss = (sg.who == i) ? D.bs
-                                   : (i < sg.who ? offd_.at({i, sg.who}).bs : offd_.at({sg.who, i}).bs);
-                for (int r = 0; r < sg.len; r += PANEL_ROWS) {
-                    PanelTile t{};
-                    t.src = src; t.sstride = ss; t.lds = lds; t.trans = trans;
-                    t.row0 = sg.row + r; t.nrows = std::min(PANEL_ROWS, sg.len - r);
-                    t.src_row0 = r0 + r;
-                    tiles.push_back(t);
-                }
+            for (int r = 0; r < nR; r += PANEL_ROWS) {
+                PanelTile t{};
+                t.src = nullptr; t.row0 = r; t.nrows = std::min(PANEL_ROWS, nR - r); t.src_row0 = r;
+                tiles.push_back(t);
             }
             const PanelTile *dt = (const PanelTile *)stage(tiles.data(), sizeof(PanelTile) * tiles.size());
-            CK(launch_panel(dt, (int)tiles.size(), s_, D.p, D.bs, m, nR, perm, dinfo, ps, Wb.p, Xb.p,
-                            Wb.bs, nR, st_));
+            CK(launch_panel(dt, (int)tiles.size(), s_, D.p, D.bs, m, nR, perm, dinfo, ps, WI.p, XI.p,
+                            WI.bs, nR, st_));
             st_acc_->launches++;
+            GemmBatch g0;
+            add_gemm(g0, gm(XI.p, XI.bs, nR, 0, WI.p, WI.bs, nR, 1, G.p, G.bs, nR, nR, nR, nR, 1.0,
+                            0.0), s_);
+            flush(g0, s_);
+            Blk Xb = alloc(R, nR, false);
+            GemmBatch g1;
+            for (auto &sg : segs) {
+                if (sg.len <= 0) continue;
+                const double *A; int lda, tA;
+                seg_as_A(sg, &A, &lda, &tA);
+                add_gemm(g1, gm(A, sg.ss, lda, tA, G.p, G.bs, nR, 0, Xb.at(sg.row, 0), Xb.bs, nR,
+                                sg.len, nR, nR, 1.0, 0.0), s_);
+            }
+            flush(g1, s_);
+            flops += 2.0 * nR * nR * nR + 2.0 * (double)R * nR * nR;
             // ---- K6: Schur updates of every target pair, one grouped launch
             GemmBatch g;
             double sch = 0.0;
             auto upd = [&](const Seg &a, const Seg &b, double *C, int64_t sC, int ldc) {
                 if (a.len <= 0 || b.len <= 0) return;
-                add_gemm(g, gm(Xb.at(a.row, 0), Xb.bs, nR, 0, Wb.at(b.row, 0), Wb.bs, nR, 1, C, sC,
-                               ldc, a.len, b.len, nR, -1.0, 1.0), s_);
+                const double *B; int ldb, tB;
+                seg_as_Bt(b, &B, &ldb, &tB);
+                add_gemm(g, gm(Xb.at(a.row, 0), Xb.bs, nR, 0, B, b.ss, ldb, tB, C, sC, ldc, a.len,
+                               b.len, nR, -1.0, 1.0), s_);
                 sch += (a.who == b.who ? 1.0 : 2.0) * (double)a.len * b.len * nR;
             };
             upd(segs[0], segs[0], D.at(nR, nR), D.bs, m);
@@ -846,7 +871,9 @@ private:
                 }
             flops += sch;
             flush(g, s_, 1);
-            release(Wb);
+            release(WI);
+            release(XI);
+            release(G);
             release(Xb);
         }
         st_acc_->flops += flops * s_;

@@ -4,16 +4,23 @@
 // Reference: gldl.py:365-378 builds Ball = [D_SR; partner slices] with
 // np.vstack, solves W = Ball[:, perm] L^{-T} with scipy solve_triangular
 // (dtrsm) and X = W D^{-1} with np.linalg.solve (a full LU of the block
-// diagonal D).  Here the gather is folded into the tile load (each tile reads
-// its rows straight from the source block, transposed when the partner block
-// is stored (i, j) with i the eliminated cluster), the permutation is applied
-// on load, the solve runs right-looking on a 32-row tile held in shared
-// memory, and D^{-1} is applied per 1x1 / 2x2 pivot block (LAPACK dsytrs
-// scaling for the 2x2 case) - mathematically identical to the reference's
-// dense solve and ~100x cheaper.
+// diagonal D).  The engine runs this kernel on the n x n identity (src ==
+// nullptr), giving W_I = P^T L^{-T} and X_I = W_I D^{-1}; the panel of every
+// partner block is then one DMMA GEMM with G = X_I W_I^T (engine.cu).  The
+// kernel still accepts real source rows (gather folded into the tile load,
+// transposed when the partner block is stored (i, j) with i eliminated).
+//
+// One CTA solves a 32-row tile for one shift: the tile lives in shared
+// memory with an odd row stride, L is staged once into shared memory packed
+// by columns (n <= PANEL_L_SMEM) so every step reads broadcast operands, and
+// the solve runs right-looking, one barrier per column.  D^{-1} is applied
+// per 1x1 / 2x2 pivot block (LAPACK dsytrs scaling for 2x2) - mathematically
+// the reference's dense solve.
 #include "common.cuh"
 
 namespace h2l {
+
+constexpr int PANEL_L_SMEM = 160;
 
 namespace {
 
@@ -24,18 +31,34 @@ __global__ void __launch_bounds__(256) panel_kernel(const PanelTile *tiles, cons
                                                     int64_t wstride, int ldw) {
     extern __shared__ __align__(16) double sm[];
     const int S = n + 1 + (n & 1);  // odd row stride -> conflict-free column access
-    double *T = sm;       // PANEL_ROWS x S
+    double *T = sm;                 // PANEL_ROWS x S
+    const bool lsm = n <= PANEL_L_SMEM;
+    double *Ls = T + PANEL_ROWS * S;  // packed strictly-lower L by columns
+    int *cs = (int *)(Ls + (lsm ? (int64_t)n * (n - 1) / 2 : 0));
     const PanelTile tl = tiles[blockIdx.x];
     const int z = blockIdx.y;
-    const double *src = tl.src + z * tl.sstride;
+    const double *src = tl.src ? tl.src + z * tl.sstride : nullptr;
     const double *Lz = L + z * lstride;
     const int *pz = perm + z * pstride;
     const double *dz = dinfo + 3 * z * pstride;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-    // ---- gather + permute
-    if (tl.trans) {
-        // panel row r = column (src_row0 + r) of src; lanes run along the row of src
+    if (lsm) {
+        // column c holds rows c+1..n-1 at Ls[cs[c] + row]; cs[c] = c*n - c(c+1)/2 - (c+1)... (row offset)
+        for (int c = threadIdx.x; c < n; c += blockDim.x) cs[c] = c * (n - 1) - (c * (c - 1)) / 2 - (c + 1);
+        __syncthreads();
+        for (int i = warp; i < n; i += 8)
+            for (int c = lane; c < i; c += 32) {
+                const bool two = dz[3 * c + 2] > 1.5 && i == c + 1;  // 2x2: L(c+1, c) = 0
+                Ls[cs[c] + i] = two ? 0.0 : Lz[(int64_t)i * ldl + c];
+            }
+    }
+    // ---- gather + permute (src == nullptr: the identity, i.e. W = P^T L^{-T})
+    if (!src) {
+        for (int r = warp; r < PANEL_ROWS; r += 8)
+            for (int c = lane; c < n; c += 32)
+                T[r * S + c] = (r < tl.nrows && pz[c] == tl.src_row0 + r) ? 1.0 : 0.0;
+    } else if (tl.trans) {
         for (int c = warp; c < n; c += 8) {
             const int pc = pz[c];
             T[lane * S + c] = lane < tl.nrows ? src[(int64_t)pc * tl.lds + tl.src_row0 + lane] : 0.0;
@@ -48,12 +71,18 @@ __global__ void __launch_bounds__(256) panel_kernel(const PanelTile *tiles, cons
     __syncthreads();
 
     // ---- forward substitution with unit-lower L (L(c+1, c) of a 2x2 pivot is D, not L)
+    double *trow = T + lane * S;
     for (int c = 0; c < n - 1; ++c) {
-        const double wc = T[lane * S + c];
-        const bool two = dz[3 * c + 2] > 1.5;
-        for (int cc = c + 1 + warp; cc < n; cc += 8) {
-            const double l = (two && cc == c + 1) ? 0.0 : __ldg(Lz + (int64_t)cc * ldl + c);
-            T[lane * S + cc] -= wc * l;
+        const double wc = trow[c];
+        if (lsm) {
+            const double *lc = Ls + cs[c];
+            for (int cc = c + 1 + warp; cc < n; cc += 8) trow[cc] -= wc * lc[cc];
+        } else {
+            const bool two = dz[3 * c + 2] > 1.5;
+            for (int cc = c + 1 + warp; cc < n; cc += 8) {
+                const double l = (two && cc == c + 1) ? 0.0 : __ldg(Lz + (int64_t)cc * ldl + c);
+                trow[cc] -= wc * l;
+            }
         }
         __syncthreads();
     }
@@ -62,18 +91,18 @@ __global__ void __launch_bounds__(256) panel_kernel(const PanelTile *tiles, cons
     if (lane < tl.nrows) {
         double *wrow = W + z * wstride + (int64_t)(tl.row0 + lane) * ldw;
         double *xrow = X + z * wstride + (int64_t)(tl.row0 + lane) * ldw;
-        for (int c = warp; c < n; c += 8) wrow[c] = T[lane * S + c];
+        for (int c = warp; c < n; c += 8) wrow[c] = trow[c];
         for (int c = warp; c < n; c += 8) {
             const double bs = dz[3 * c + 2];
             if (bs > 1.5) {
                 const double e = dz[3 * c + 1];
                 const double a1 = dz[3 * c] / e, a2 = dz[3 * c + 3] / e;
                 const double den = a1 * a2 - 1.0;
-                const double b1 = T[lane * S + c] / e, b2 = T[lane * S + c + 1] / e;
+                const double b1 = trow[c] / e, b2 = trow[c + 1] / e;
                 xrow[c] = (a2 * b1 - b2) / den;
                 xrow[c + 1] = (a1 * b2 - b1) / den;
             } else if (bs > 0.5) {
-                xrow[c] = T[lane * S + c] / dz[3 * c];
+                xrow[c] = trow[c] / dz[3 * c];
             }
         }
     }
@@ -81,14 +110,18 @@ __global__ void __launch_bounds__(256) panel_kernel(const PanelTile *tiles, cons
 
 }  // namespace
 
-size_t panel_smem_bytes(int n) { return sizeof(double) * PANEL_ROWS * (size_t)(n + 2); }
+size_t panel_smem_bytes(int n) {
+    size_t b = sizeof(double) * PANEL_ROWS * (size_t)(n + 2);
+    if (n <= PANEL_L_SMEM) b += sizeof(double) * (size_t)n * (n - 1) / 2 + sizeof(int) * (size_t)n;
+    return b;
+}
 
 cudaError_t launch_panel(const PanelTile *dev_tiles, int ntiles, int nshift, const double *L,
                          int64_t lstride, int ldl, int n, const int *perm, const double *dinfo,
                          int64_t pstride, double *W, double *X, int64_t wstride, int ldw,
                          cudaStream_t st) {
     if (ntiles <= 0 || nshift <= 0 || n <= 0) return cudaSuccess;
-    size_t sm = panel_smem_bytes(n);
+    const size_t sm = panel_smem_bytes(n);
     cudaError_t e =
         cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;

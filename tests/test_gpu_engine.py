@@ -167,3 +167,27 @@ def test_cfg1_multisection_many_eigenvalues(cfg1):
     w = z["eigs"]
     for e in ests:
         assert abs(e.value - w[e.k - 1]) <= 1e-8 + 1e-12 * abs(w[e.k - 1]), e.k
+
+
+def test_cfg1_multisection_over_nccl_world1(cfg1):
+    # the multi-GPU driver (NCCL all-gather of counts) on the one GPU of the box
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2311_08618_b200.multigpu import multisection_distributed
+
+    H, z = cfg1
+    iv = tuple(float(v) for v in z["interval"])
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        ests, ev = multisection_distributed(H, [1024, 1], iv, 1e-8, per_rank=63)
+    finally:
+        dist.destroy_process_group()
+    assert ests[0].value == float(z["estimate"][0])
+    assert abs(ests[1].value - z["eigs"][0]) <= 1e-8
+    assert ev.rounds > 0 and ev.world == 1
