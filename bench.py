@@ -8,10 +8,10 @@ uniform points in [0,1]^3 (seed 0, Morton order), leaf 128, eta = 1,
 eps = 1e-8.  This is the only configuration whose input (the H2 matrix) can
 be built today (configs 2-5 need the GPU construction that SURVEY.md §8f
 lists next).  A step = one shift-batched sweep of the generalized LDL^T over
-S shifts (default 64) spread over the spectrum; `value` = shifts factorized
+S shifts (default 256) spread over the spectrum; `value` = shifts factorized
 per second over K timed steps (device time, CUDA events on the engine's
 stream, max over ranks); inputs (the uploaded H payload, 17.8 MB, and its
-s-batched working copies, 1.1 GB per step) are resident in HBM and exceed L2,
+s-batched working copies, 4.6 GB per step at S = 256) are resident in HBM and exceed L2,
 so no flush is needed.  `e2e` = the same metric through the public API
 `inertia_batch(H, mus)` with host shift lists and host counts (H2D of the
 shifts and D2H of the counts inside the timed region, wall clock).
@@ -239,6 +239,8 @@ def run_ours(args):
     ms = 0.0
     ms_schur = 0.0
     schur_flops = 0.0
+    schur_bytes = 0.0
+    gemm_exec = 0.0
     flops = 0.0
     launches = 0
     ok = True
@@ -248,6 +250,8 @@ def run_ours(args):
         ms += st["ms_total"]
         ms_schur += st["ms_schur"]
         schur_flops += st["schur_flops"]
+        schur_bytes += st["bytes"]
+        gemm_exec += st["gemm_flops_exec"]
         flops += st["flops"]
         launches += st["launches"]
         if k == 0:  # spot-check against the exact spectrum (rank-0 H2: exact matrix)
@@ -301,7 +305,13 @@ def run_ours(args):
                      "frac": (achieved / peak) if achieved else None, "traffic": None,
                      "peak_source": "measured in-run: cuBLAS DGEMM fp64 8192^3 best of 5 "
                                     "(MEASURED_PEAKS.json has no fp64 figure)",
-                     "schur_share_of_step": ms_schur / ms if ms else None},
+                     "schur_share_of_step": ms_schur / ms if ms else None,
+                     "algorithmic_flops_per_eval": schur_flops / (S * args.steps),
+                     "algorithmic_bytes_per_eval": schur_bytes / (S * args.steps),
+                     "flops_rule": "SURVEY.md §8d: Schur 2 nR [sum_{a<b} l_a l_b + 1/2 sum_a l_a^2] "
+                                   "per elimination step, live rows only"},
+        "step_rates": {"algorithmic_tflops": flops / t_dev / 1e12 / max(1, 1),
+                       "dmma_executed_tflops": gemm_exec / (ms / 1e3) / 1e12 if ms else None},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * S,
                 "d2h_bytes_per_step": (3 * 8 + 4) * S},
         "gpu_launches": launches,
@@ -312,7 +322,7 @@ def run_ours(args):
                        "multisection_evals": mest.inertia_evals,
                        "value": est.value, "multisection_equal": mest.value == est.value,
                        "abs_err_vs_eigvalsh": abs(est.value - float(eigs[1023]))},
-        "flops_per_step": flops / args.steps,
+        "algorithmic_flops_per_step": flops / args.steps,
     }
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample(args.cpu_seconds)
@@ -328,7 +338,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg1", choices=["cfg1"])
-    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -94,13 +94,14 @@ typedef struct h2l_stats {
     int64_t rank_added;
     int64_t max_front;
     double dropped_fro;   /* summed over shifts */
-    double flops;         /* algorithmic fp64 flops of the call (all shifts) */
-    double bytes;         /* algorithmic HBM bytes of the call (all shifts) */
+    double flops;         /* algorithmic fp64 flops of the call (all shifts, survey §8d) */
+    double bytes;         /* algorithmic HBM bytes of the Schur updates (targets r+w, X/W reads) */
     double ms_total;      /* device time of the call (CUDA events) */
     double ms_schur;      /* device time inside the Schur-update GEMM launches */
     double ms_bk;         /* device time inside the BK launches */
     int64_t launches;     /* kernels launched by the call */
-    double schur_flops;   /* flops of the Schur-update GEMM launches */
+    double schur_flops;   /* algorithmic flops of the Schur updates (survey §8d formula) */
+    double gemm_flops_exec; /* flops executed by all DMMA GEMM launches (2MNK) */
 } h2l_stats;
 
 int h2l_create(h2l_engine **engine, int device);

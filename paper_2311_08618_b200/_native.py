@@ -52,6 +52,7 @@ class Stats(ctypes.Structure):
         ("bytes", ctypes.c_double), ("ms_total", ctypes.c_double),
         ("ms_schur", ctypes.c_double), ("ms_bk", ctypes.c_double),
         ("launches", ctypes.c_int64), ("schur_flops", ctypes.c_double),
+        ("gemm_flops_exec", ctypes.c_double),
     ]
 
     def as_dict(self):

@@ -380,8 +380,8 @@ private:
             if (timed) CK(cudaEventRecord(next_event(), st_));
             if (st_acc_) {
                 st_acc_->launches++;
-                st_acc_->flops += b.flops;
-                if (kind == 1) st_acc_->schur_flops += b.flops;
+                st_acc_->gemm_flops_exec += b.flops;
+                if (kind == 2) st_acc_->flops += b.flops;  // rotations / merges: executed == algorithmic
             }
         }
         b = GemmBatch{};
@@ -664,7 +664,10 @@ private:
                     st_acc_->dropped_fro += dr[z];
                 }
             st_acc_->recompressions++;
-            st_acc_->flops += 4.0 * c * nR * (double)std::max(t, 1) * s_;
+            {   // algorithmic QR of G (nR x c), survey §8d: 2 c nR^2 - 2/3 nR^3 (for c >= nR)
+                const double a = std::max(c, nR), b = std::min(c, nR);
+                st_acc_->flops += (2.0 * a * b * b - 2.0 / 3.0 * b * b * b) * s_;
+            }
             if (t > 0) {
                 CK(launch_pqr(GT.p, GT.bs, c, nR, nR, tau, piv, used, norms, vs, cs, d_tol_, d_rank_,
                               d_dropped_, d_active, t, s_, st_));
@@ -717,7 +720,7 @@ private:
                 repl.push_back({&B, N});
             }
         }
-        flush(g1, s_);
+        flush(g1, s_, 2);
         flush(c1);
         col_transform(Y, Z, Tr.p, Tr.bs, nR, nS, t, g2, c2);
         // couplings: zero-pad by t rows/cols (gldl.py:324-330)
@@ -728,7 +731,7 @@ private:
             if (C.p && N.p) add_copy(c2, cp(C.p, C.bs, C.cols, N.p, N.bs, N.cols, C.rows, C.cols));
             crepl.push_back({&C, N});
         }
-        flush(g2, s_);
+        flush(g2, s_, 2);
         flush(c2);
         release(diag_[i]);
         release(Y);
@@ -822,10 +825,11 @@ private:
                                 sg.len, nR, nR, 1.0, 0.0), s_);
             }
             flush(g1, s_);
-            flops += 2.0 * nR * nR * nR + 2.0 * (double)R * nR * nR;
+            // algorithmic panel work (survey §8d): TRSM R nR^2 + D-scale R nR
+            flops += (double)R * nR * nR + (double)R * nR;
             // ---- K6: Schur updates of every target pair, one grouped launch
             GemmBatch g;
-            double sch = 0.0;
+            double sch = 0.0, sch_bytes = 16.0 * (double)R * nR;  // X and W read once
             auto upd = [&](const Seg &a, const Seg &b, double *C, int64_t sC, int ldc) {
                 if (a.len <= 0 || b.len <= 0) return;
                 const double *B; int ldb, tB;
@@ -833,6 +837,7 @@ private:
                 add_gemm(g, gm(Xb.at(a.row, 0), Xb.bs, nR, 0, B, b.ss, ldb, tB, C, sC, ldc, a.len,
                                b.len, nR, -1.0, 1.0), s_);
                 sch += (a.who == b.who ? 1.0 : 2.0) * (double)a.len * b.len * nR;
+                sch_bytes += 16.0 * (double)a.len * b.len;  // target read + write
             };
             upd(segs[0], segs[0], D.at(nR, nR), D.bs, m);
             for (size_t x = 1; x < segs.size(); ++x) {
@@ -870,6 +875,8 @@ private:
                     upd(a, b, T->at(a.lo, b.lo), T->bs, T->cols);
                 }
             flops += sch;
+            st_acc_->schur_flops += sch * s_;
+            st_acc_->bytes += sch_bytes * s_;
             flush(g, s_, 1);
             release(WI);
             release(XI);
@@ -1105,8 +1112,8 @@ private:
             st_acc_->fill_blocks++;
             zeros.push_back(kv.second);
         }
-        flush(g1, s_);
-        flush(g2, s_);
+        flush(g1, s_, 2);
+        flush(g2, s_, 2);
         for (auto &b : tmps) release(b);
         for (auto &b : zeros) release(b);
         for (auto &b : raw) release(b);
@@ -1295,3 +1302,75 @@ int h2l_bk_inertia(int device, const double *a, int64_t n, int32_t count, const 
 const char *h2l_version(void) { return "h2ldl 0.1 sm_100a"; }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ internal tooling
+// Not part of the ABI (absent from h2ldl.h): micro-benchmark of the DMMA GEMM
+// tile variants on a Schur-shaped grouped workload (tools/gemm_bench.py).
+namespace h2l {
+int gemm_variant_tiles(int v, int M, int N);
+void launch_gemm_variant(int v, const GemmTask *dev_tasks, const int *dev_tile_prefix, int ntasks,
+                         int total_tiles, int nshift, cudaStream_t st);
+}
+
+extern "C" int h2l_internal_gemm_bench(int device, int variant, int M, int N, int K, int ntasks,
+                                       int nshift, int reps, double *ms_out, double *maxdiff_out) {
+    return guarded(nullptr, [&] {
+        CK(cudaSetDevice(device));
+        const int64_t sa = (int64_t)M * K, sb = (int64_t)N * K, sc = (int64_t)M * N;
+        const int64_t per = (sa + sb + sc) * ntasks;
+        double *buf, *ref;
+        CK(cudaMalloc(&buf, sizeof(double) * per * nshift));
+        CK(cudaMalloc(&ref, sizeof(double) * sc * ntasks * nshift));
+        std::vector<double> h(per * nshift);
+        uint64_t x = 88172645463325252ull;
+        for (auto &v : h) { x ^= x << 13; x ^= x >> 7; x ^= x << 17; v = (double)(x % 2001) / 1000.0 - 1.0; }
+        CK(cudaMemcpy(buf, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+        std::vector<h2l::GemmTask> tasks(ntasks);
+        for (int t = 0; t < ntasks; ++t) {
+            h2l::GemmTask &g = tasks[t];
+            g = h2l::GemmTask{};
+            g.A = buf + t * sa; g.B = buf + ntasks * sa + t * sb; g.C = buf + ntasks * (sa + sb) + t * sc;
+            g.sA = g.sB = g.sC = per;
+            g.M = M; g.N = N; g.K = K; g.lda = K; g.ldb = K; g.ldc = N; g.tA = 0; g.tB = 1;
+            g.alpha = -1.0; g.beta = 1.0;
+        }
+        auto run = [&](int v, int nrep, float *ms) {
+            std::vector<int> pre(ntasks);
+            int tiles = 0;
+            for (int t = 0; t < ntasks; ++t) { pre[t] = tiles; tiles += h2l::gemm_variant_tiles(v, M, N); }
+            h2l::GemmTask *dt; int *dp;
+            CK(cudaMalloc(&dt, sizeof(h2l::GemmTask) * ntasks));
+            CK(cudaMalloc(&dp, sizeof(int) * ntasks));
+            CK(cudaMemcpy(dt, tasks.data(), sizeof(h2l::GemmTask) * ntasks, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dp, pre.data(), sizeof(int) * ntasks, cudaMemcpyHostToDevice));
+            cudaEvent_t e0, e1;
+            cudaEventCreate(&e0); cudaEventCreate(&e1);
+            h2l::launch_gemm_variant(v, dt, dp, ntasks, tiles, nshift, 0);  // warm
+            CK(cudaDeviceSynchronize());
+            cudaEventRecord(e0);
+            for (int r = 0; r < nrep; ++r) h2l::launch_gemm_variant(v, dt, dp, ntasks, tiles, nshift, 0);
+            cudaEventRecord(e1);
+            CK(cudaEventSynchronize(e1));
+            cudaEventElapsedTime(ms, e0, e1);
+            cudaEventDestroy(e0); cudaEventDestroy(e1);
+            cudaFree(dt); cudaFree(dp);
+        };
+        // correctness: one launch of `variant` vs one of variant 0 from the same inputs
+        const size_t cbytes = sizeof(double) * sc * ntasks;
+        std::vector<double> c0(sc * ntasks), c1(sc * ntasks);
+        double *Cz = buf + ntasks * (sa + sb);
+        float ms = 0.f;
+        CK(cudaMemcpy(ref, Cz, cbytes, cudaMemcpyDeviceToDevice));
+        run(0, 0, &ms);
+        CK(cudaMemcpy(c0.data(), Cz, cbytes, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(Cz, ref, cbytes, cudaMemcpyDeviceToDevice));
+        run(variant, 0, &ms);
+        CK(cudaMemcpy(c1.data(), Cz, cbytes, cudaMemcpyDeviceToHost));
+        double md = 0.0;
+        for (size_t q = 0; q < c0.size(); ++q) md = std::max(md, std::fabs(c0[q] - c1[q]));
+        run(variant, reps, &ms);
+        *ms_out = ms / std::max(1, reps);
+        *maxdiff_out = md;
+        cudaFree(buf); cudaFree(ref);
+    });
+}

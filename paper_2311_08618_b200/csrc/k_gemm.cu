@@ -8,24 +8,27 @@
 // recompression rotations (gldl.py:313-331), the merge congruences Q^T R Q
 // (gldl.py:523-545) and the skeleton prologue Q^T A Q (compress.py:99-127).
 //
-// Tiling: one CTA computes a 64x64 tile of one task for one shift with 4
-// warps (2x2), each warp a 32x32 sub-tile = 4x4 DMMA fragments.  The C
-// fragments of the read-modify-write target are prefetched into registers
-// before the K loop (the K extent of a Schur update is only n_R ~ 100-400,
-// so an exposed epilogue load would dominate).  K advances in chunks of 16 through a 3-stage cp.async
-// pipeline (global -> shared without register staging; out-of-range
-// elements zero-filled by the copy), shared rows padded to 20 doubles so
-// fragment reads are conflict-free.  Tasks are flattened into one grid
-// through a tile prefix array: thousands of small blocks of one elimination
-// step go out in a single launch; gridDim.y enumerates shifts.
+// Tiling (template GemmCfg): a CTA computes a BM x BN tile of one task for
+// one shift; warps are laid out (BM/WM) x (BN/WN), each warp owns a WM x WN
+// sub-tile of (WM/8) x (WN/8) DMMA fragments.  K advances in chunks of 16
+// through a STAGES-deep cp.async pipeline (global -> shared without register
+// staging; out-of-range elements zero-filled by the copy), shared rows padded
+// to 20 doubles so fragment reads are conflict-free.  The production tile
+// (64x64, 2x2 warps of 32x32, 2 stages, <= 128 registers so 4 CTAs = 16
+// warps share an SM) was picked with tools/gemm_bench.py: on the Schur
+// shapes of configs 1-2 (K = n_R = 128-192) occupancy beats deeper
+// pipelines and larger warp tiles; the epilogue loads C with all loads of a
+// fragment row issued before its stores (other resident CTAs hide the
+// latency; staging C in shared memory costs occupancy).  Tasks are flattened
+// into one grid through a tile prefix array: thousands of small blocks of one
+// elimination step go out in a single launch; gridDim.y enumerates shifts.
 #include "common.cuh"
 
 namespace h2l {
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, SK = BK + 4, STAGES = 3;
-constexpr int FM = BM / 16;  // DMMA fragments per warp along M (warp tile (BM/2) x 32)
+constexpr int BK = 16, SK = BK + 4;
 
 __device__ __forceinline__ int find_task(const int *prefix, int ntasks, int tile) {
     int lo = 0, hi = ntasks - 1;
@@ -51,27 +54,37 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, bool CSTAGE_ = true, int MINB_ = 1>
+struct GemmCfg {
+    static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_;
+    static constexpr bool CSTAGE = CSTAGE_;  // prefetch C into shared memory
+    static constexpr int MINB = MINB_;       // min resident CTAs per SM (register cap)
+    static constexpr int WARPS = (BM / WM) * (BN / WN);
+    static constexpr int THREADS = WARPS * 32;
+    static constexpr int FM = WM / 8, FN = WN / 8;
+    static constexpr int CS = BN + 1;  // padded row stride of the staged C tile
+    static constexpr size_t SMEM =
+        sizeof(double) * ((size_t)STAGES * (BM + BN) * SK + (CSTAGE ? (size_t)BM * CS : 0));
+};
+
 // Stage the ROWS x 16 chunk of op(X) starting at (row0, k0) into S[ROWS][SK].
 // op: element (r, k) = trans ? X[k*ld + r] : X[r*ld + k]
-template <int ROWS>
+template <int ROWS, int THREADS>
 __device__ __forceinline__ void load_chunk(double (*S)[SK], const double *X, int ld, int trans,
                                            int rows, int K, int row0, int k0, int tid) {
-    constexpr int PER = ROWS * BK / 128;
+    constexpr int TOTAL = ROWS * BK;
     if (!trans) {
-        const int k = k0 + (tid & 15);
 #pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            const int rl = (tid >> 4) + 8 * i;
-            const int r = row0 + rl;
+        for (int e = tid; e < TOTAL; e += THREADS) {
+            const int rl = e >> 4, kl = e & 15;
+            const int r = row0 + rl, k = k0 + kl;
             const bool ok = r < rows && k < K;
-            cp_async8(&S[rl][tid & 15], ok ? X + (int64_t)r * ld + k : X, ok);
+            cp_async8(&S[rl][kl], ok ? X + (int64_t)r * ld + k : X, ok);
         }
     } else {
-        constexpr int RSTEP = 128 / ROWS;  // k rows covered per pass
 #pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            const int rl = tid % ROWS;
-            const int kl = tid / ROWS + RSTEP * i;
+        for (int e = tid; e < TOTAL; e += THREADS) {
+            const int rl = e % ROWS, kl = e / ROWS;
             const int r = row0 + rl, k = k0 + kl;
             const bool ok = r < rows && k < K;
             cp_async8(&S[rl][kl], ok ? X + (int64_t)k * ld + r : X, ok);
@@ -79,11 +92,15 @@ __device__ __forceinline__ void load_chunk(double (*S)[SK], const double *X, int
     }
 }
 
-__global__ void __launch_bounds__(128) gemm_kernel(const GemmTask *tasks, const int *prefix,
-                                                   int ntasks) {
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_kernel(const GemmTask *tasks,
+                                                            const int *prefix, int ntasks) {
+    constexpr int BM = Cfg::BM, BN = Cfg::BN, STAGES = Cfg::STAGES, FM = Cfg::FM, FN = Cfg::FN;
+    constexpr int THREADS = Cfg::THREADS, CS = Cfg::CS;
     extern __shared__ __align__(16) double gsm[];
     double (*As)[BM][SK] = reinterpret_cast<double (*)[BM][SK]>(gsm);
     double (*Bs)[BN][SK] = reinterpret_cast<double (*)[BN][SK]>(gsm + STAGES * BM * SK);
+    double *Cs = gsm + STAGES * (BM + BN) * SK;
 
     const int t = find_task(prefix, ntasks, blockIdx.x);
     const GemmTask tk = tasks[t];
@@ -98,36 +115,34 @@ __global__ void __launch_bounds__(128) gemm_kernel(const GemmTask *tasks, const 
 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
-    const int wm = (warp >> 1) * (BM / 2), wn = (warp & 1) * 32;
-    // opB element (k, n): tB=1 -> B[n*ldb+k] (rows of B are n) ; tB=0 -> B[k*ldb+n]
+    constexpr int WCOLS = BN / Cfg::WN;
+    const int wm = (warp / WCOLS) * Cfg::WM, wn = (warp % WCOLS) * Cfg::WN;
     const int b_trans = tk.tB ? 0 : 1;
+    const bool rd = tk.beta != 0.0;
 
-    double acc[FM][4][2];
+    // C prefetch (own cp.async group, completes with the first K stage)
+    if (Cfg::CSTAGE && rd) {
+        for (int e = tid; e < BM * BN; e += THREADS) {
+            const int rl = e / BN, cl = e % BN;
+            const int r = m0 + rl, c = n0 + cl;
+            const bool ok = r < tk.M && c < tk.N;
+            cp_async8(&Cs[rl * CS + cl], ok ? C + (int64_t)r * tk.ldc + c : C, ok);
+        }
+    }
+    cp_commit();
+
+    double acc[FM][FN][2];
 #pragma unroll
     for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    // prefetch the C fragments (beta != 0): the loads overlap the whole K loop
-    const bool rd = tk.beta != 0.0;
-    double cpre[FM][4][2];
-#pragma unroll
-    for (int i = 0; i < FM; ++i) {
-        const int r = m0 + wm + i * 8 + (lane >> 2);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int c = n0 + wn + j * 8 + 2 * (lane & 3);
-            const double *p = C + (int64_t)r * tk.ldc + c;
-            cpre[i][j][0] = (rd && r < tk.M && c < tk.N) ? p[0] : 0.0;
-            cpre[i][j][1] = (rd && r < tk.M && c + 1 < tk.N) ? p[1] : 0.0;
-        }
-    }
+        for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     const int nk = (tk.K + BK - 1) / BK;
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
         if (s < nk) {
-            load_chunk<BM>(As[s], A, tk.lda, tk.tA, tk.M, tk.K, m0, s * BK, tid);
-            load_chunk<BN>(Bs[s], B, tk.ldb, b_trans, tk.N, tk.K, n0, s * BK, tid);
+            load_chunk<BM, THREADS>(As[s], A, tk.lda, tk.tA, tk.M, tk.K, m0, s * BK, tid);
+            load_chunk<BN, THREADS>(Bs[s], B, tk.ldb, b_trans, tk.N, tk.K, n0, s * BK, tid);
         }
         cp_commit();
     }
@@ -137,56 +152,120 @@ __global__ void __launch_bounds__(128) gemm_kernel(const GemmTask *tasks, const 
         const int nxt = kc + STAGES - 1;
         if (nxt < nk) {
             const int sl = nxt % STAGES;
-            load_chunk<BM>(As[sl], A, tk.lda, tk.tA, tk.M, tk.K, m0, nxt * BK, tid);
-            load_chunk<BN>(Bs[sl], B, tk.ldb, b_trans, tk.N, tk.K, n0, nxt * BK, tid);
+            load_chunk<BM, THREADS>(As[sl], A, tk.lda, tk.tA, tk.M, tk.K, m0, nxt * BK, tid);
+            load_chunk<BN, THREADS>(Bs[sl], B, tk.ldb, b_trans, tk.N, tk.K, n0, nxt * BK, tid);
         }
         cp_commit();
         const int cur = kc % STAGES;
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 4) {
-            double af[FM], bf[4];
+            double af[FM], bf[FN];
 #pragma unroll
             for (int i = 0; i < FM; ++i) af[i] = As[cur][wm + i * 8 + (lane >> 2)][kk + (lane & 3)];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) bf[j] = Bs[cur][wn + j * 8 + (lane >> 2)][kk + (lane & 3)];
+            for (int j = 0; j < FN; ++j) bf[j] = Bs[cur][wn + j * 8 + (lane >> 2)][kk + (lane & 3)];
 #pragma unroll
             for (int i = 0; i < FM; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+                for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         }
     }
     cp_wait<0>();
+    __syncthreads();
 
-    // epilogue: C = alpha*acc + beta*C (C already in registers)
+    // epilogue: C = alpha*acc + beta*C
+    if (Cfg::CSTAGE) {
 #pragma unroll
-    for (int i = 0; i < FM; ++i) {
-        const int r = m0 + wm + i * 8 + (lane >> 2);
-        if (r >= tk.M) continue;
-        double *crow = C + (int64_t)r * tk.ldc;
+        for (int i = 0; i < FM; ++i) {
+            const int rl = wm + i * 8 + (lane >> 2);
+            const int r = m0 + rl;
+            if (r >= tk.M) continue;
+            double *crow = C + (int64_t)r * tk.ldc;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int c = n0 + wn + j * 8 + 2 * (lane & 3);
-            if (c < tk.N) crow[c] = tk.alpha * acc[i][j][0] + tk.beta * cpre[i][j][0];
-            if (c + 1 < tk.N) crow[c + 1] = tk.alpha * acc[i][j][1] + tk.beta * cpre[i][j][1];
+            for (int j = 0; j < FN; ++j) {
+                const int cl = wn + j * 8 + 2 * (lane & 3);
+                const int c = n0 + cl;
+                if (c < tk.N)
+                    crow[c] = tk.alpha * acc[i][j][0] + (rd ? tk.beta * Cs[rl * CS + cl] : 0.0);
+                if (c + 1 < tk.N)
+                    crow[c + 1] = tk.alpha * acc[i][j][1] + (rd ? tk.beta * Cs[rl * CS + cl + 1] : 0.0);
+            }
+        }
+    } else {
+        // all loads of a fragment row group before its stores (no aliasing stalls)
+#pragma unroll
+        for (int i = 0; i < FM; ++i) {
+            const int r = m0 + wm + i * 8 + (lane >> 2);
+            if (r >= tk.M) continue;
+            double *crow = C + (int64_t)r * tk.ldc;
+            double cv[FN][2];
+#pragma unroll
+            for (int j = 0; j < FN; ++j) {
+                const int c = n0 + wn + j * 8 + 2 * (lane & 3);
+                cv[j][0] = (rd && c < tk.N) ? crow[c] : 0.0;
+                cv[j][1] = (rd && c + 1 < tk.N) ? crow[c + 1] : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < FN; ++j) {
+                const int c = n0 + wn + j * 8 + 2 * (lane & 3);
+                if (c < tk.N) crow[c] = tk.alpha * acc[i][j][0] + tk.beta * cv[j][0];
+                if (c + 1 < tk.N) crow[c + 1] = tk.alpha * acc[i][j][1] + tk.beta * cv[j][1];
+            }
         }
     }
 }
 
-constexpr size_t GEMM_SMEM = sizeof(double) * STAGES * (BM + BN) * SK;
+// production configuration (chosen with tools/gemm_bench.py)
+using Prod = GemmCfg<64, 64, 32, 32, 2, false, 4>;
+
+template <class Cfg>
+void launch_cfg(const GemmTask *dev_tasks, const int *dev_tile_prefix, int ntasks,
+                int total_tiles, int nshift, cudaStream_t st) {
+    cudaFuncSetAttribute(gemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Cfg::SMEM);
+    dim3 grid(total_tiles, nshift);
+    gemm_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(dev_tasks, dev_tile_prefix, ntasks);
+}
 
 }  // namespace
 
 int gemm_tiles(int M, int N) {
     if (M <= 0 || N <= 0) return 0;
-    return ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+    return ((M + Prod::BM - 1) / Prod::BM) * ((N + Prod::BN - 1) / Prod::BN);
 }
 
 void launch_gemm(const GemmTask *dev_tasks, const int *dev_tile_prefix, int ntasks,
                  int total_tiles, int nshift, cudaStream_t st) {
     if (ntasks <= 0 || total_tiles <= 0 || nshift <= 0) return;
-    cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
-    dim3 grid(total_tiles, nshift);
-    gemm_kernel<<<grid, 128, GEMM_SMEM, st>>>(dev_tasks, dev_tile_prefix, ntasks);
+    launch_cfg<Prod>(dev_tasks, dev_tile_prefix, ntasks, total_tiles, nshift, st);
+}
+
+// ---- variants for tools/gemm_bench.py (the tile prefix must use the variant's tiling)
+using V0 = GemmCfg<64, 64, 32, 32, 3>;
+using V1 = GemmCfg<64, 128, 32, 64, 3>;
+using V2 = GemmCfg<64, 64, 32, 32, 2, false, 5>;
+using V3 = GemmCfg<64, 64, 32, 32, 3, false, 3>;
+using V4 = GemmCfg<64, 64, 32, 32, 2, false, 4>;
+using V5 = GemmCfg<128, 64, 32, 32, 2, false, 2>;
+using V6 = GemmCfg<64, 64, 32, 16, 2, false, 6>;
+using V7 = GemmCfg<128, 64, 32, 32, 3, false, 2>;
+#define H2L_VARIANTS(X) X(0, V0) X(1, V1) X(2, V2) X(3, V3) X(4, V4) X(5, V5) X(6, V6) X(7, V7)
+
+int gemm_variant_tiles(int v, int M, int N) {
+    if (M <= 0 || N <= 0) return 0;
+#define X(id, C) \
+    if (v == id) return ((M + C::BM - 1) / C::BM) * ((N + C::BN - 1) / C::BN);
+    H2L_VARIANTS(X)
+#undef X
+    return 0;
+}
+
+void launch_gemm_variant(int v, const GemmTask *dev_tasks, const int *dev_tile_prefix, int ntasks,
+                         int total_tiles, int nshift, cudaStream_t st) {
+#define X(id, C) \
+    if (v == id) launch_cfg<C>(dev_tasks, dev_tile_prefix, ntasks, total_tiles, nshift, st);
+    H2L_VARIANTS(X)
+#undef X
 }
 
 }  // namespace h2l
