@@ -19,7 +19,7 @@ import numpy as np
 from .errors import NativeError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libh2ldl.so")
+LIB_PATH = os.environ.get("H2L_LIB", os.path.join(HERE, "libh2ldl.so"))
 
 H2L_OK = 0
 H2L_SHIFT_OK = 0

@@ -8,6 +8,9 @@
 #pragma once
 
 #include <cstdint>
+#include <mutex>
+#include <set>
+#include <utility>
 #include <cuda_runtime.h>
 
 namespace h2l {
@@ -64,6 +67,31 @@ struct BkJob {
     double *dinfo;   // [shift][3*pstride]: d, e (2x2 off-diagonal), block size
     int64_t pstride;
 };
+
+// Opt a kernel into the largest dynamic shared memory once per (kernel, device),
+// before its first launch.  Setting function attributes while another host
+// thread launches the same kernel is avoided entirely (waves run concurrently).
+template <class F>
+inline cudaError_t smem_optin(F *f) {
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(mu);
+    const auto key = std::make_pair((const void *)f, dev);
+    if (done.count(key)) return cudaSuccess;
+    int optin = 0;
+    e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e != cudaSuccess) return e;
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, f);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             optin - (int)fa.sharedSizeBytes);
+    if (e == cudaSuccess) done.insert(key);
+    return e;
+}
 
 // ---- launchers (stream-ordered; return the launch error)
 int copy_tiles(int rows, int cols);

@@ -30,6 +30,9 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <mutex>
+#include <memory>
+#include <thread>
 #include <set>
 #include <stdexcept>
 #include <string>
@@ -54,6 +57,8 @@ struct CudaFail : std::runtime_error {
     } while (0)
 
 using Pair = std::pair<int, int>;
+
+
 
 static inline int64_t pad4(int64_t v) { return (v + 3) / 4 * 4; }
 
@@ -85,22 +90,27 @@ struct Cl {
     int m = 0, nR = 0, nS = 0, r0 = 0;
 };
 
-class Engine {
+class Wave {
 public:
-    explicit Engine(int device) : dev_(device) {
+    explicit Wave(int device) : dev_(device) {
         CK(cudaSetDevice(dev_));
         cudaDeviceProp prop;
         CK(cudaGetDeviceProperties(&prop, dev_));
         if (prop.major < 10) throw CudaFail(H2L_ENODEV, "device is not sm_100 class");
         CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
-        cudaMemPool_t pool;
-        CK(cudaDeviceGetDefaultMemPool(&pool, dev_));
+        // private stream-ordered pool per wave: blocks never migrate between the
+        // streams of concurrent waves
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev_;
+        CK(cudaMemPoolCreate(&pool_, &props));
         uint64_t thr = UINT64_MAX;
-        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        CK(cudaMemPoolSetAttribute(pool_, cudaMemPoolAttrReleaseThreshold, &thr));
         stage_.init(size_t(64) << 20);
         for (int k = 0; k < 2; ++k) CK(cudaEventCreate(&ev_call_[k]));
     }
-    ~Engine() {
+    ~Wave() {
         cudaSetDevice(dev_);
         cudaStreamSynchronize(st_);
         free_payload();
@@ -108,6 +118,7 @@ public:
         for (int k = 0; k < 2; ++k) cudaEventDestroy(ev_call_[k]);
         stage_.release();
         cudaStreamDestroy(st_);
+        cudaMemPoolDestroy(pool_);
     }
 
     void set_option(const std::string &k, int64_t v) {
@@ -204,9 +215,32 @@ public:
         if (stats) *stats = acc;
     }
 
+    // share the uploaded payload of `o` (read-only; `o` keeps ownership)
+    void adopt(const Wave &o) {
+        CK(cudaSetDevice(dev_));
+        free_payload();
+        n_ = o.n_; depth_ = o.depth_; kind_ = o.kind_; eps_ = o.eps_; scale0_ = o.scale0_;
+        ranges_ = o.ranges_; boff_ = o.boff_; brank_ = o.brank_; bdim_ = o.bdim_;
+        dense_ = o.dense_; lowrank_ = o.lowrank_; deferred_ = o.deferred_; coup_off_ = o.coup_off_;
+        arena_ = o.arena_; skel_ = o.skel_; skel_diag_ = o.skel_diag_; skel_off_ = o.skel_off_;
+        max_batch_ = o.max_batch_; time_kernels_ = o.time_kernels_;
+        owns_payload_ = false;
+        uploaded_ = o.uploaded_;
+    }
+    cudaStream_t stream() const { return st_; }
+    int max_batch() const { return max_batch_; }
+    // run one wave (<= max_batch shifts) and accumulate into acc (stream-ordered, synchronous)
+    void run(const double *mu, int s, int64_t *counts, int32_t *status, h2l_stats &acc) {
+        if (!uploaded_) throw CudaFail(H2L_ESTATE, "h2l_inertia before h2l_upload");
+        CK(cudaSetDevice(dev_));
+        run_wave(mu, s, counts, status, acc);
+    }
+
     std::string err;
 
 private:
+    bool owns_payload_ = true;
+    cudaMemPool_t pool_ = nullptr;
     int dev_;
     cudaStream_t st_ = nullptr;
     Staging stage_;
@@ -257,10 +291,13 @@ private:
     }
 
     void free_payload() {
-        if (arena_) cudaFree(arena_);
-        if (skel_) cudaFree(skel_);
+        if (owns_payload_) {
+            if (arena_) cudaFree(arena_);
+            if (skel_) cudaFree(skel_);
+        }
         arena_ = skel_ = nullptr;
         uploaded_ = false;
+        owns_payload_ = true;
     }
 
     const void *stage(const void *src, size_t nbytes) {
@@ -280,24 +317,75 @@ private:
         stage_.off += bytes;
         return d;
     }
+    void dbg_sync(const char *what = "") {
+        if (guard_mode()) {
+            CK(cudaStreamSynchronize(st_));
+            last_launch_ = what;
+            check_guards();
+        }
+    }
     void sync() {
         CK(cudaStreamSynchronize(st_));
         stage_.off = 0;
     }
 
+    // debug (H2L_DEBUG_GUARD): every block gets GUARD doubles of 0xff canary on both
+    // sides, checked after every launch by dbg_sync()
+    static constexpr int64_t GUARD = 512;
+    static bool guard_mode() {
+        static const bool g = getenv("H2L_DEBUG_GUARD") != nullptr;
+        return g;
+    }
+    std::map<double *, int64_t> live_;  // interior pointer -> interior doubles
+    std::string last_launch_;
+    void check_guards() {
+        std::vector<unsigned char> buf(sizeof(double) * GUARD);
+        for (auto &kv : live_) {
+            for (int side = 0; side < 2; ++side) {
+                const double *g = side == 0 ? kv.first - GUARD : kv.first + kv.second;
+                CK(cudaMemcpy(buf.data(), g, buf.size(), cudaMemcpyDeviceToHost));
+                for (size_t q = 0; q < buf.size(); ++q)
+                    if (buf[q] != 0xff) {
+                        fprintf(stderr, "GUARD %p: %s overwrote %s guard of block %p (+%lld doubles) at byte %zu after [%s]\n",
+                                (void *)this, side ? "tail" : "head", side ? "tail" : "head", (void *)kv.first,
+                                (long long)kv.second, q, last_launch_.c_str());
+                        CK(cudaMemset((void *)g, 0xff, buf.size()));
+                        break;
+                    }
+            }
+        }
+    }
     Blk alloc(int rows, int cols, bool zero) {
         Blk b;
         b.rows = rows;
         b.cols = cols;
         b.bs = pad4((int64_t)rows * cols);
         if (rows > 0 && cols > 0) {
-            CK(cudaMallocAsync((void **)&b.p, sizeof(double) * b.bs * s_, st_));
+            if (guard_mode()) {
+                double *base;
+                const int64_t inner = b.bs * s_;
+                CK(cudaMallocFromPoolAsync((void **)&base, sizeof(double) * (inner + 2 * GUARD), pool_, st_));
+                CK(cudaMemsetAsync(base, 0xff, sizeof(double) * (inner + 2 * GUARD), st_));
+                b.p = base + GUARD;
+                live_[b.p] = inner;
+            } else {
+                CK(cudaMallocFromPoolAsync((void **)&b.p, sizeof(double) * b.bs * s_, pool_, st_));
+            }
             if (zero) CK(cudaMemsetAsync(b.p, 0, sizeof(double) * b.bs * s_, st_));
         }
         return b;
     }
     void release(Blk &b) {
-        if (b.p) CK(cudaFreeAsync(b.p, st_));
+        if (b.p) {
+            if (guard_mode()) {
+                CK(cudaStreamSynchronize(st_));
+                check_guards();
+                live_.erase(b.p);
+                CK(cudaFreeAsync(b.p - GUARD, st_));
+            } else {
+                CK(cudaFreeAsync(b.p, st_));
+            }
+        }
         b = Blk{};
     }
 
@@ -339,6 +427,7 @@ private:
             const int *dp = (const int *)stage(b.pre.data(), sizeof(int) * b.pre.size());
             launch_copy_prefixed(dt, dp, (int)b.t.size(), b.tiles, s_ ? s_ : 1, mu, st_);
             CK(cudaGetLastError());
+            dbg_sync("copy");
             if (st_acc_) st_acc_->launches++;
         }
         b = CopyBatch{};
@@ -377,6 +466,7 @@ private:
             if (timed) CK(cudaEventRecord(mark(1), st_));
             launch_gemm(dt, dp, (int)b.t.size(), b.tiles, nshift, st_);
             CK(cudaGetLastError());
+            dbg_sync(kind == 1 ? "gemm-schur" : (kind == 2 ? "gemm-rot" : "gemm-panel"));
             if (timed) CK(cudaEventRecord(next_event(), st_));
             if (st_acc_) {
                 st_acc_->launches++;
@@ -430,12 +520,12 @@ private:
         ev_marks_.clear();
         std::vector<double> tol(s);
         for (int z = 0; z < s; ++z) tol[z] = eps_ * (scale0_ + std::fabs(mu[z]));
-        CK(cudaMallocAsync((void **)&d_mu_, sizeof(double) * s, st_));
-        CK(cudaMallocAsync((void **)&d_tol_, sizeof(double) * s, st_));
-        CK(cudaMallocAsync((void **)&d_dropped_, sizeof(double) * s, st_));
-        CK(cudaMallocAsync((void **)&d_counts_, sizeof(int64_t) * 3 * s, st_));
-        CK(cudaMallocAsync((void **)&d_status_, sizeof(int) * s, st_));
-        CK(cudaMallocAsync((void **)&d_rank_, sizeof(int) * s, st_));
+        CK(cudaMallocFromPoolAsync((void **)&d_mu_, sizeof(double) * s, pool_, st_));
+        CK(cudaMallocFromPoolAsync((void **)&d_tol_, sizeof(double) * s, pool_, st_));
+        CK(cudaMallocFromPoolAsync((void **)&d_dropped_, sizeof(double) * s, pool_, st_));
+        CK(cudaMallocFromPoolAsync((void **)&d_counts_, sizeof(int64_t) * 3 * s, pool_, st_));
+        CK(cudaMallocFromPoolAsync((void **)&d_status_, sizeof(int) * s, pool_, st_));
+        CK(cudaMallocFromPoolAsync((void **)&d_rank_, sizeof(int) * s, pool_, st_));
         CK(cudaMemcpyAsync(d_mu_, stage(mu, sizeof(double) * s), sizeof(double) * s,
                            cudaMemcpyDeviceToDevice, st_));
         CK(cudaMemcpyAsync(d_tol_, stage(tol.data(), sizeof(double) * s), sizeof(double) * s,
@@ -641,12 +731,12 @@ private:
             const int64_t vs = pad4(nR), cs = pad4(c);
             double *tau, *norms;
             int *piv, *used;
-            CK(cudaMallocAsync((void **)&tau, sizeof(double) * vs * s_, st_));
-            CK(cudaMallocAsync((void **)&piv, sizeof(int) * vs * s_, st_));
-            CK(cudaMallocAsync((void **)&used, sizeof(int) * cs * s_, st_));
-            CK(cudaMallocAsync((void **)&norms, sizeof(double) * cs * s_, st_));
+            CK(cudaMallocFromPoolAsync((void **)&tau, sizeof(double) * vs * s_, pool_, st_));
+            CK(cudaMallocFromPoolAsync((void **)&piv, sizeof(int) * vs * s_, pool_, st_));
+            CK(cudaMallocFromPoolAsync((void **)&used, sizeof(int) * cs * s_, pool_, st_));
+            CK(cudaMallocFromPoolAsync((void **)&norms, sizeof(double) * cs * s_, pool_, st_));
             int *d_active;
-            CK(cudaMallocAsync((void **)&d_active, sizeof(int) * s_, st_));
+            CK(cudaMallocFromPoolAsync((void **)&d_active, sizeof(int) * s_, pool_, st_));
             activity_from_status(d_active);
             CK(launch_pqr(GT.p, GT.bs, c, nR, nR, tau, piv, used, norms, vs, cs, d_tol_, d_rank_,
                           d_dropped_, d_active, -1, s_, st_));
@@ -769,8 +859,8 @@ private:
         const int64_t ps = pad4(nR);
         int *perm;
         double *dinfo;
-        CK(cudaMallocAsync((void **)&perm, sizeof(int) * ps * s_, st_));
-        CK(cudaMallocAsync((void **)&dinfo, sizeof(double) * 3 * ps * s_, st_));
+        CK(cudaMallocFromPoolAsync((void **)&perm, sizeof(int) * ps * s_, pool_, st_));
+        CK(cudaMallocFromPoolAsync((void **)&dinfo, sizeof(double) * 3 * ps * s_, pool_, st_));
         bk_launch(D.p, D.bs, m, nR, perm, dinfo, ps);
         // ---- panel segments (live rows only)
         std::vector<int> partners;
@@ -810,6 +900,7 @@ private:
             const PanelTile *dt = (const PanelTile *)stage(tiles.data(), sizeof(PanelTile) * tiles.size());
             CK(launch_panel(dt, (int)tiles.size(), s_, D.p, D.bs, m, nR, perm, dinfo, ps, WI.p, XI.p,
                             WI.bs, nR, st_));
+            dbg_sync("panel");
             st_acc_->launches++;
             GemmBatch g0;
             add_gemm(g0, gm(XI.p, XI.bs, nR, 0, WI.p, WI.bs, nR, 1, G.p, G.bs, nR, nR, nR, nR, 1.0,
@@ -904,8 +995,9 @@ private:
         const BkJob *dj = (const BkJob *)stage(&jb, sizeof(jb));
         const int64_t scr = bk_scratch_doubles(n);
         double *scratch = nullptr;
-        if (scr) CK(cudaMallocAsync((void **)&scratch, sizeof(double) * scr * s_, st_));
+        if (scr) CK(cudaMallocFromPoolAsync((void **)&scratch, sizeof(double) * scr * s_, pool_, st_));
         CK(launch_bk_engine(dj, 1, s_, n, d_counts_, d_status_, scratch, scr, st_));
+        dbg_sync("bk");
         st_acc_->launches++;
         if (scratch) CK(cudaFreeAsync(scratch, st_));
     }
@@ -916,8 +1008,8 @@ private:
         const int64_t ps = pad4(n);
         int *perm;
         double *dinfo;
-        CK(cudaMallocAsync((void **)&perm, sizeof(int) * ps * s_, st_));
-        CK(cudaMallocAsync((void **)&dinfo, sizeof(double) * 3 * ps * s_, st_));
+        CK(cudaMallocFromPoolAsync((void **)&perm, sizeof(int) * ps * s_, pool_, st_));
+        CK(cudaMallocFromPoolAsync((void **)&dinfo, sizeof(double) * 3 * ps * s_, pool_, st_));
         bk_launch(root.p, root.bs, root.cols, n, perm, dinfo, ps);
         st_acc_->flops += (double)n * n * n / 3.0 * s_;
         CK(cudaFreeAsync(perm, st_));
@@ -1042,7 +1134,7 @@ private:
                 continue;
             }
             double *qp;
-            CK(cudaMallocAsync((void **)&qp, sizeof(double) * (int64_t)mp * mp, st_));
+            CK(cudaMallocFromPoolAsync((void **)&qp, sizeof(double) * (int64_t)mp * mp, pool_, st_));
             CK(cudaMemsetAsync(qp, 0, sizeof(double) * (int64_t)mp * mp, st_));
             Qown.push_back(qp);
             Q[p] = qp;
@@ -1148,10 +1240,125 @@ __global__ void active_kernel(const int *status, int *active, int s) {
     int z = blockIdx.x * blockDim.x + threadIdx.x;
     if (z < s) active[z] = status[z] == 0;
 }
-void Engine::activity_from_status(int *d_active) {
+void Wave::activity_from_status(int *d_active) {
     active_kernel<<<(s_ + 127) / 128, 128, 0, st_>>>(d_status_, d_active, s_);
     CK(cudaGetLastError());
 }
+}  // namespace h2l
+
+// ------------------------------------------------------------ concurrent waves
+// The engine splits a call into waves of <= max_batch shifts and runs up to
+// `concurrency` waves at once, each on its own stream driven by its own host
+// thread.  Within one wave the elimination steps are a dependent chain of
+// latency-bound launches (BK, panel) and throughput-bound ones (DMMA GEMMs);
+// a second wave in flight fills the SMs the first one leaves idle.
+namespace h2l {
+static void merge_stats(h2l_stats &a, const h2l_stats &b) {
+    a.fill_blocks = std::max(a.fill_blocks, b.fill_blocks);
+    a.recompressions = std::max(a.recompressions, b.recompressions);
+    a.rank_added = std::max(a.rank_added, b.rank_added);
+    a.max_front = std::max(a.max_front, b.max_front);
+    a.dropped_fro += b.dropped_fro;
+    a.flops += b.flops;
+    a.bytes += b.bytes;
+    a.ms_schur += b.ms_schur;
+    a.ms_bk += b.ms_bk;
+    a.launches += b.launches;
+    a.schur_flops += b.schur_flops;
+    a.gemm_flops_exec += b.gemm_flops_exec;
+}
+
+class Engine {
+public:
+    explicit Engine(int device) : dev_(device) {
+        waves_.emplace_back(new Wave(device));
+        CK(cudaEventCreate(&ev_[0]));
+        CK(cudaEventCreate(&ev_[1]));
+    }
+    ~Engine() {
+        cudaSetDevice(dev_);
+        for (size_t k = 1; k < waves_.size(); ++k) waves_[k].reset();  // borrowers first
+        waves_.clear();
+        cudaEventDestroy(ev_[0]);
+        cudaEventDestroy(ev_[1]);
+    }
+    void set_option(const std::string &k, int64_t v) {
+        if (k == "concurrency") {
+            concurrency_ = (int)std::max<int64_t>(1, std::min<int64_t>(8, v));
+            return;
+        }
+        for (auto &w : waves_) w->set_option(k, v);
+    }
+    void upload(const h2l_plan *pl) {
+        waves_[0]->upload(pl);
+        for (size_t k = 1; k < waves_.size(); ++k) waves_[k]->adopt(*waves_[0]);
+    }
+    void inertia(const double *mu, int s, int64_t *counts, int32_t *status, h2l_stats *stats) {
+        CK(cudaSetDevice(dev_));
+        const int mb = waves_[0]->max_batch();
+        const int nw = (s + mb - 1) / mb;
+        const int C = std::min(concurrency_, nw);
+        while ((int)waves_.size() < C) {
+            waves_.emplace_back(new Wave(dev_));
+            waves_.back()->adopt(*waves_[0]);
+        }
+        std::vector<h2l_stats> acc(C);
+        for (auto &a : acc) a = h2l_stats{};
+        cudaStream_t s0 = waves_[0]->stream();
+        CK(cudaEventRecord(ev_[0], s0));
+        for (int t = 1; t < C; ++t) CK(cudaStreamWaitEvent(waves_[t]->stream(), ev_[0], 0));
+        auto work = [&](int t) {
+            for (int w = t; w < nw; w += C) {
+                const int w0 = w * mb, ws = std::min(mb, s - w0);
+                waves_[t]->run(mu + w0, ws, counts + 3 * (int64_t)w0, status + w0, acc[t]);
+            }
+        };
+        if (C == 1) {
+            work(0);
+        } else {
+            std::vector<std::thread> th;
+            std::vector<std::string> errs(C);
+            std::vector<int> codes(C, 0);
+            for (int t = 0; t < C; ++t)
+                th.emplace_back([&, t] {
+                    try {
+                        cudaSetDevice(dev_);
+                        work(t);
+                    } catch (const CudaFail &x) {
+                        codes[t] = x.code;
+                        errs[t] = x.what();
+                    } catch (const std::exception &x) {
+                        codes[t] = H2L_EINVAL;
+                        errs[t] = x.what();
+                    }
+                });
+            for (auto &x : th) x.join();
+            for (int t = 0; t < C; ++t)
+                if (codes[t]) throw CudaFail(codes[t], errs[t]);
+            for (int t = 1; t < C; ++t) {
+                cudaEvent_t e;
+                CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                CK(cudaEventRecord(e, waves_[t]->stream()));
+                CK(cudaStreamWaitEvent(s0, e, 0));
+                CK(cudaEventDestroy(e));
+            }
+        }
+        CK(cudaEventRecord(ev_[1], s0));
+        CK(cudaEventSynchronize(ev_[1]));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
+        h2l_stats tot{};
+        for (auto &a : acc) merge_stats(tot, a);
+        tot.ms_total = ms;
+        if (stats) *stats = tot;
+    }
+
+private:
+    int dev_;
+    int concurrency_ = 2;
+    cudaEvent_t ev_[2];
+    std::vector<std::unique_ptr<Wave>> waves_;
+};
 }  // namespace h2l
 
 // =================================================================== C ABI
@@ -1372,5 +1579,108 @@ extern "C" int h2l_internal_gemm_bench(int device, int variant, int M, int N, in
         *ms_out = ms / std::max(1, reps);
         *maxdiff_out = md;
         cudaFree(buf); cudaFree(ref);
+    });
+}
+
+// Debug: production GEMM vs a naive reference kernel on a Schur-shaped
+// grouped workload; returns the max abs difference (tools/gemm_concurrency.py).
+namespace h2l {
+__global__ void naive_gemm_kernel(const GemmTask *tasks, int ntasks) {
+    const int t = blockIdx.x, z = blockIdx.y;
+    if (t >= ntasks) return;
+    const GemmTask tk = tasks[t];
+    const double *A = tk.A + z * tk.sA, *B = tk.B + z * tk.sB;
+    double *C = tk.C + z * tk.sC;
+    for (int e = threadIdx.x; e < tk.M * tk.N; e += blockDim.x) {
+        const int r = e / tk.N, c = e % tk.N;
+        double s = 0.0;
+        for (int k = 0; k < tk.K; ++k) {
+            const double a = tk.tA ? A[(int64_t)k * tk.lda + r] : A[(int64_t)r * tk.lda + k];
+            const double b = tk.tB ? B[(int64_t)c * tk.ldb + k] : B[(int64_t)k * tk.ldb + c];
+            s += a * b;
+        }
+        C[(int64_t)r * tk.ldc + c] = tk.alpha * s + tk.beta * C[(int64_t)r * tk.ldc + c];
+    }
+}
+}  // namespace h2l
+
+extern "C" int h2l_internal_gemm_check(int device, int M, int N, int K, int ntasks, int nshift,
+                                       int reps, double *maxdiff_out) {
+    return guarded(nullptr, [&] {
+        CK(cudaSetDevice(device));
+        cudaStream_t st;
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        const int64_t sa = (int64_t)M * K, sb = (int64_t)N * K, sc = (int64_t)M * N;
+        const int64_t per = (sa + sb + 2 * sc) * ntasks;
+        double *buf;
+        CK(cudaMalloc(&buf, sizeof(double) * per * nshift));
+        std::vector<double> h(per * nshift);
+        uint64_t x = 0x9E3779B97F4A7C15ull ^ (uint64_t)(M * 131 + N * 7 + ntasks);
+        for (auto &v : h) { x ^= x << 13; x ^= x >> 7; x ^= x << 17; v = (double)(x % 2001) / 1000.0 - 1.0; }
+        CK(cudaMemcpy(buf, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+        std::vector<h2l::GemmTask> t1(ntasks), t2(ntasks);
+        std::vector<int> pre(ntasks);
+        int tiles = 0;
+        for (int t = 0; t < ntasks; ++t) {
+            h2l::GemmTask g{};
+            g.A = buf + t * sa; g.B = buf + ntasks * sa + t * sb;
+            g.sA = g.sB = g.sC = per;
+            g.M = M; g.N = N; g.K = K; g.lda = K; g.ldb = K; g.ldc = N; g.tA = 0; g.tB = 1;
+            g.alpha = -1.0; g.beta = 1.0;
+            g.C = buf + ntasks * (sa + sb) + t * sc;
+            t1[t] = g;
+            g.C = buf + ntasks * (sa + sb + sc) + t * sc;
+            t2[t] = g;
+            pre[t] = tiles;
+            tiles += h2l::gemm_tiles(M, N);
+        }
+        h2l::GemmTask *d1, *d2; int *dp;
+        CK(cudaMalloc(&d1, sizeof(h2l::GemmTask) * ntasks));
+        CK(cudaMalloc(&d2, sizeof(h2l::GemmTask) * ntasks));
+        CK(cudaMalloc(&dp, sizeof(int) * ntasks));
+        CK(cudaMemcpy(d1, t1.data(), sizeof(h2l::GemmTask) * ntasks, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(d2, t2.data(), sizeof(h2l::GemmTask) * ntasks, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dp, pre.data(), sizeof(int) * ntasks, cudaMemcpyHostToDevice));
+        // both C copies start equal (copy C1 -> C2)
+        for (int z = 0; z < nshift; ++z)
+            CK(cudaMemcpyAsync(buf + z * per + ntasks * (sa + sb + sc), buf + z * per + ntasks * (sa + sb),
+                               sizeof(double) * sc * ntasks, cudaMemcpyDeviceToDevice, st));
+        CK(cudaStreamSynchronize(st));
+        double md = 0.0;
+        for (int r = 0; r < reps; ++r) {
+            h2l::launch_gemm(d1, dp, ntasks, tiles, nshift, st);
+            cudaError_t e1 = cudaGetLastError();
+            h2l::naive_gemm_kernel<<<dim3(ntasks, nshift), 256, 0, st>>>(d2, ntasks);
+            cudaError_t e2 = cudaGetLastError();
+            cudaError_t e3 = cudaStreamSynchronize(st);
+            if (e1 || e2 || e3)
+                fprintf(stderr, "LAUNCH rep %d: gemm=%s naive=%s sync=%s\n", r, cudaGetErrorString(e1),
+                        cudaGetErrorString(e2), cudaGetErrorString(e3));
+        }
+        std::vector<double> c1(sc * ntasks * nshift), c2(sc * ntasks * nshift);
+        for (int z = 0; z < nshift; ++z) {
+            CK(cudaMemcpy(c1.data() + z * sc * ntasks, buf + z * per + ntasks * (sa + sb),
+                          sizeof(double) * sc * ntasks, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(c2.data() + z * sc * ntasks, buf + z * per + ntasks * (sa + sb + sc),
+                          sizeof(double) * sc * ntasks, cudaMemcpyDeviceToHost));
+        }
+        int64_t nbad = 0;
+        for (size_t q = 0; q < c1.size(); ++q) {
+            const double d = std::fabs(c1[q] - c2[q]);
+            md = std::max(md, d);
+            if (d > 1e-9) {
+                if (nbad < 12) {
+                    const int64_t z = q / (sc * ntasks), rem = q % (sc * ntasks);
+                    const int64_t t = rem / sc, e = rem % sc;
+                    fprintf(stderr, "BAD z=%lld task=%lld r=%lld c=%lld got=%g want=%g\n", (long long)z,
+                            (long long)t, (long long)(e / N), (long long)(e % N), c1[q], c2[q]);
+                }
+                ++nbad;
+            }
+        }
+        if (nbad) fprintf(stderr, "BAD total %lld of %zu\n", (long long)nbad, c1.size());
+        *maxdiff_out = md;
+        cudaFree(buf); cudaFree(d1); cudaFree(d2); cudaFree(dp);
+        cudaStreamDestroy(st);
     });
 }

@@ -215,13 +215,16 @@ __device__ __forceinline__ int bk_core(Packed A, int n, double tol, double *w0, 
         if (absakk >= __dmul_rn(alpha, colmax)) {
             kp = k;
         } else {
+            // every decision input is read before the barrier inside block_max:
+            // past it, thread 0 may already be interchanging (kk,kk) <-> (kp,kp)
+            const double aii = fabs(A.at(imax, imax));
             double r = 0.0;
             for (int j = k + tid; j < imax; j += nthr) r = fmax(r, fabs(A.at(imax, j)));
             for (int i = imax + 1 + tid; i < n; i += nthr) r = fmax(r, fabs(A.at(i, imax)));
             const double rowmax = block_max(r, sh.red_d);
             if (__dmul_rn(absakk, rowmax) >= __dmul_rn(__dmul_rn(alpha, colmax), colmax)) {
                 kp = k;
-            } else if (fabs(A.at(imax, imax)) >= __dmul_rn(alpha, rowmax)) {
+            } else if (aii >= __dmul_rn(alpha, rowmax)) {
                 kp = imax;
             } else {
                 kp = imax;
@@ -521,14 +524,12 @@ cudaError_t launch_bk_engine(const BkJob *dev_jobs, int njobs, int nshift, int n
     const size_t sm = bk_smem_bytes(nmax);
     dim3 grid(njobs, nshift);
     if (nmax <= BK_SMEM_MAX) {
-        cudaError_t e = cudaFuncSetAttribute(bk_engine_kernel<true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaError_t e = smem_optin(bk_engine_kernel<true>);
         if (e != cudaSuccess) return e;
         bk_engine_kernel<true><<<grid, BK_THREADS, sm, st>>>(dev_jobs, nmax, (long long *)counts,
                                                              status, scratch, scratch_stride);
     } else {
-        cudaError_t e = cudaFuncSetAttribute(bk_engine_kernel<false>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaError_t e = smem_optin(bk_engine_kernel<false>);
         if (e != cudaSuccess) return e;
         bk_engine_kernel<false><<<grid, BK_THREADS, sm, st>>>(dev_jobs, nmax, (long long *)counts,
                                                               status, scratch, scratch_stride);
@@ -542,13 +543,11 @@ cudaError_t launch_bk_kat(double *a, int n, int count, const double *tol, int64_
     if (n > BK_NMAX) return cudaErrorInvalidValue;
     const size_t sm = bk_smem_bytes(n);
     if (n <= BK_SMEM_MAX) {
-        cudaError_t e = cudaFuncSetAttribute(bk_kat_kernel<true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaError_t e = smem_optin(bk_kat_kernel<true>);
         if (e != cudaSuccess) return e;
         bk_kat_kernel<true><<<count, BK_THREADS, sm, st>>>(a, n, tol, ipiv, info, scratch);
     } else {
-        cudaError_t e = cudaFuncSetAttribute(bk_kat_kernel<false>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaError_t e = smem_optin(bk_kat_kernel<false>);
         if (e != cudaSuccess) return e;
         bk_kat_kernel<false><<<count, BK_THREADS, sm, st>>>(a, n, tol, ipiv, info, scratch);
     }

@@ -221,8 +221,7 @@ using Prod = GemmCfg<64, 64, 32, 32, 2, false, 4>;
 template <class Cfg>
 void launch_cfg(const GemmTask *dev_tasks, const int *dev_tile_prefix, int ntasks,
                 int total_tiles, int nshift, cudaStream_t st) {
-    cudaFuncSetAttribute(gemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Cfg::SMEM);
+    smem_optin(gemm_kernel<Cfg>);
     dim3 grid(total_tiles, nshift);
     gemm_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(dev_tasks, dev_tile_prefix, ntasks);
 }

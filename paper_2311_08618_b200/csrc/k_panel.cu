@@ -24,12 +24,54 @@ constexpr int PANEL_L_SMEM = 160;
 
 namespace {
 
+// Register-resident right-looking solve of a 32-row tile: lane = row, warp w
+// owns columns w + 8 j (j < NJ) of its row in registers; per column c the
+// owning warp publishes T(:, c) through a double-buffered shared vector, one
+// barrier per column, and every thread updates its own later columns with L
+// read from shared memory.  Result written back to T.
+template <int NJ>
+__device__ __forceinline__ void solve_regs(double *T, int S, const double *Ls, const int *cs, int n,
+                                           double (*colbuf)[PANEL_ROWS]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double r[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        const int c = warp + 8 * j;
+        r[j] = c < n ? T[lane * S + c] : 0.0;
+    }
+    for (int c = 0; c < n - 1; ++c) {
+        if ((c & 7) == warp) {
+            const int jc = c >> 3;
+            double v = 0.0;
+#pragma unroll
+            for (int j = 0; j < NJ; ++j)
+                if (j == jc) v = r[j];
+            colbuf[c & 1][lane] = v;
+        }
+        __syncthreads();
+        const double wc = colbuf[c & 1][lane];
+        const double *lc = Ls + cs[c];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            const int cc = warp + 8 * j;
+            if (cc > c && cc < n) r[j] -= wc * lc[cc];
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        const int c = warp + 8 * j;
+        if (c < n) T[lane * S + c] = r[j];
+    }
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(256) panel_kernel(const PanelTile *tiles, const double *L,
                                                     int64_t lstride, int ldl, int n,
                                                     const int *perm, const double *dinfo,
                                                     int64_t pstride, double *W, double *X,
                                                     int64_t wstride, int ldw) {
     extern __shared__ __align__(16) double sm[];
+    __shared__ double colbuf[2][PANEL_ROWS];
     const int S = n + 1 + (n & 1);  // odd row stride -> conflict-free column access
     double *T = sm;                 // PANEL_ROWS x S
     const bool lsm = n <= PANEL_L_SMEM;
@@ -72,19 +114,20 @@ __global__ void __launch_bounds__(256) panel_kernel(const PanelTile *tiles, cons
 
     // ---- forward substitution with unit-lower L (L(c+1, c) of a 2x2 pivot is D, not L)
     double *trow = T + lane * S;
-    for (int c = 0; c < n - 1; ++c) {
-        const double wc = trow[c];
-        if (lsm) {
-            const double *lc = Ls + cs[c];
-            for (int cc = c + 1 + warp; cc < n; cc += 8) trow[cc] -= wc * lc[cc];
-        } else {
+    if (lsm && n <= 32) solve_regs<4>(T, S, Ls, cs, n, colbuf);
+    else if (lsm && n <= 64) solve_regs<8>(T, S, Ls, cs, n, colbuf);
+    else if (lsm && n <= 128) solve_regs<16>(T, S, Ls, cs, n, colbuf);
+    else if (lsm) solve_regs<20>(T, S, Ls, cs, n, colbuf);
+    else {
+        for (int c = 0; c < n - 1; ++c) {
+            const double wc = trow[c];
             const bool two = dz[3 * c + 2] > 1.5;
             for (int cc = c + 1 + warp; cc < n; cc += 8) {
                 const double l = (two && cc == c + 1) ? 0.0 : __ldg(Lz + (int64_t)cc * ldl + c);
                 trow[cc] -= wc * l;
             }
+            __syncthreads();
         }
-        __syncthreads();
     }
 
     // ---- write W, then X = W D^{-1}
@@ -123,7 +166,7 @@ cudaError_t launch_panel(const PanelTile *dev_tiles, int ntiles, int nshift, con
     if (ntiles <= 0 || nshift <= 0 || n <= 0) return cudaSuccess;
     const size_t sm = panel_smem_bytes(n);
     cudaError_t e =
-        cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        smem_optin(panel_kernel);
     if (e != cudaSuccess) return e;
     dim3 grid(ntiles, nshift);
     panel_kernel<<<grid, 256, sm, st>>>(dev_tiles, L, lstride, ldl, n, perm, dinfo, pstride, W, X,

@@ -14,7 +14,8 @@ STEPS = int(os.environ.get("STEPS", "2"))
 H = build_cfg1()
 (lo, hi), eigs = cfg1_interval()
 eng = _native.engine_for(H, 0)
-eng.set_option("max_batch", S)
+eng.set_option("max_batch", int(os.environ.get("MB", S)))
+eng.set_option("concurrency", int(os.environ.get("C", "2")))
 for k in range(STEPS):
     mus = shifts_for(lo, hi, S, 100 + k, 0)
     c, st, stats = ldl_counts_array(H, mus)
