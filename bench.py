@@ -151,11 +151,14 @@ def run_reference(args):
         return
     import multiprocessing as mp
 
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    # spawn (not fork): a forked child inherits the parent's OpenBLAS thread pool
+    # in a broken state and can deadlock on its first BLAS call
+    for var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[var] = "1"
     cores = os.cpu_count() or 1
     (lo, hi), _ = cfg1_interval()
-    ctx = mp.get_context("fork")
-    with ctx.Pool(cores, initializer=lambda: os.environ.update(OPENBLAS_NUM_THREADS="1")) as pool:
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(cores) as pool:
         # warm the per-process skeleton caches / imports
         pool.map(_ref_worker, [([0.0],)] * cores)
         per = 1  # shifts per worker per step: one factorization each (~0.5 s)
