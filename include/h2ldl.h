@@ -102,6 +102,10 @@ typedef struct h2l_stats {
     int64_t launches;     /* kernels launched by the call */
     double schur_flops;   /* algorithmic flops of the Schur updates (survey §8d formula) */
     double gemm_flops_exec; /* flops executed by all DMMA GEMM launches (2MNK) */
+    double ms_kind[8];    /* device ms per launch kind (time_kernels=1): 0 panel GEMMs,
+                             1 Schur GEMM, 2 rotation/merge GEMMs, 3 BK, 4 panel solve,
+                             5 copies, 6 recompression QR, 7 unused */
+    double ms_host;       /* wall-clock ms of the call on the host */
 } h2l_stats;
 
 int h2l_create(h2l_engine **engine, int device);

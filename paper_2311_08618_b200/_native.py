@@ -52,11 +52,14 @@ class Stats(ctypes.Structure):
         ("bytes", ctypes.c_double), ("ms_total", ctypes.c_double),
         ("ms_schur", ctypes.c_double), ("ms_bk", ctypes.c_double),
         ("launches", ctypes.c_int64), ("schur_flops", ctypes.c_double),
-        ("gemm_flops_exec", ctypes.c_double),
+        ("gemm_flops_exec", ctypes.c_double), ("ms_kind", ctypes.c_double * 8),
+        ("ms_host", ctypes.c_double),
     ]
 
     def as_dict(self):
-        return {name: getattr(self, name) for name, _ in self._fields_}
+        d = {name: getattr(self, name) for name, _ in self._fields_}
+        d["ms_kind"] = list(self.ms_kind)
+        return d
 
 
 SYMBOLS = ("h2l_create", "h2l_destroy", "h2l_last_error", "h2l_upload", "h2l_inertia",
@@ -150,9 +153,54 @@ class DeviceEngine:
         return counts, status, st.as_dict()
 
 
+def _device_plan(org):
+    """Plan over the device arena of a gpu_build.construct_device matrix (no copies)."""
+    tree, st = org.tree, org.structure
+    depth = tree.depth
+    nodes = (1 << (depth + 1)) - 1
+    off = org._arena_offsets
+    ranges = np.array([r for lv in tree.ranges for r in lv], dtype=np.int64).reshape(-1)
+    nleaf = 1 << depth
+    diag_off = np.array([off[("D", i)] for i in range(nleaf)], dtype=np.int64)
+    dense = np.array(st.dense, dtype=np.int32).reshape(-1, 2)
+    dense_off = np.array([off[("O", (i, j))] for i, j in st.dense], dtype=np.int64)
+    low = [(l, i, j) for l in sorted(st.lowrank) for i, j in st.lowrank[l]]
+    low_off = np.array([off[("C", k)] for k in low], dtype=np.int64)
+    lowrank = np.array(low, dtype=np.int32).reshape(-1, 3)
+    dfr = [(l, i, j) for l in sorted(st.deferred) for i, j in st.deferred[l]]
+    deferred = np.array(dfr, dtype=np.int32).reshape(-1, 3)
+    brank = np.full(nodes, -1, dtype=np.int32)
+    bdim = np.zeros(nodes, dtype=np.int32)
+    boff = np.full(nodes, -1, dtype=np.int64)
+    for (l, i), bs in org.bases.items():
+        nd = (1 << l) - 1 + i
+        brank[nd] = bs.rank
+        bdim[nd] = bs.m
+        if bs.m:
+            boff[nd] = off[("B", (l, i))]
+    arena = org._arena
+    keep = [ranges, dense, lowrank, deferred, brank, bdim, boff, diag_off, dense_off, low_off,
+            arena]
+    plan = Plan(
+        n=tree.n, depth=depth, kind=KIND[st.kind], n_dense=len(dense), n_lowrank=len(low),
+        n_deferred=len(dfr), eps=float(org.eps), scale0=float(org.scale0()),
+        ranges=_ptr(ranges, _i64p), dense=_ptr(dense, _i32p), lowrank=_ptr(lowrank, _i32p),
+        deferred=_ptr(deferred, _i32p), basis_rank=_ptr(brank, _i32p),
+        basis_dim=_ptr(bdim, _i32p), basis_off=_ptr(boff, _i64p),
+        diag_off=_ptr(diag_off, _i64p), dense_off=_ptr(dense_off, _i64p),
+        lowrank_off=_ptr(low_off, _i64p),
+        arena=ctypes.cast(ctypes.c_void_p(arena.data_ptr()), _f64p), arena_len=arena.numel())
+    return plan, keep
+
+
 def build_plan(H):
-    """Flatten origin(H) into an h2l_plan (returns the struct and the arrays it points to)."""
+    """Flatten origin(H) into an h2l_plan (returns the struct and the arrays it points to).
+
+    Host payloads are concatenated into one numpy arena; a device-built H
+    (gpu_build.construct_device) passes its device arena as is."""
     org = H.origin()
+    if getattr(org, "_arena", None) is not None:
+        return _device_plan(org)
     tree, st = org.tree, org.structure
     depth = tree.depth
     nodes = (1 << (depth + 1)) - 1

@@ -26,6 +26,7 @@
 // the reference carries its (exactly zero) redundant rows through the
 // products (gldl.py:365-409); skipping them changes no value.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -156,7 +157,11 @@ public:
         for (int e = 0; e < pl->n_deferred; ++e)
             deferred_[pl->deferred[3 * e]].push_back({pl->deferred[3 * e + 1], pl->deferred[3 * e + 2]});
         CK(cudaMalloc(&arena_, sizeof(double) * std::max<int64_t>(1, pl->arena_len)));
-        CK(cudaMemcpy(arena_, pl->arena, sizeof(double) * pl->arena_len, cudaMemcpyHostToDevice));
+        // host or device arena (unified addressing); stream-ordered on st_ and synced
+        // before any kernel reads it
+        CK(cudaMemcpyAsync(arena_, pl->arena, sizeof(double) * pl->arena_len, cudaMemcpyDefault,
+                           st_));
+        CK(cudaStreamSynchronize(st_));
         const int L = depth_;
         const int nleaf = 1 << L;
         // ---- skeleton prologue (K1): S = Q^T A Q, shift independent (compress.py:99-127)
@@ -425,7 +430,10 @@ private:
         if (!b.t.empty()) {
             const CopyTask *dt = (const CopyTask *)stage(b.t.data(), sizeof(CopyTask) * b.t.size());
             const int *dp = (const int *)stage(b.pre.data(), sizeof(int) * b.pre.size());
-            launch_copy_prefixed(dt, dp, (int)b.t.size(), b.tiles, s_ ? s_ : 1, mu, st_);
+            {
+                Timed tm(this, 5);
+                launch_copy_prefixed(dt, dp, (int)b.t.size(), b.tiles, s_ ? s_ : 1, mu, st_);
+            }
             CK(cudaGetLastError());
             dbg_sync("copy");
             if (st_acc_) st_acc_->launches++;
@@ -462,12 +470,12 @@ private:
         if (!b.t.empty()) {
             const GemmTask *dt = (const GemmTask *)stage(b.t.data(), sizeof(GemmTask) * b.t.size());
             const int *dp = (const int *)stage(b.pre.data(), sizeof(int) * b.pre.size());
-            const bool timed = time_kernels_ && kind == 1;
-            if (timed) CK(cudaEventRecord(mark(1), st_));
-            launch_gemm(dt, dp, (int)b.t.size(), b.tiles, nshift, st_);
+            {
+                Timed tm(this, kind);
+                launch_gemm(dt, dp, (int)b.t.size(), b.tiles, nshift, st_);
+            }
             CK(cudaGetLastError());
             dbg_sync(kind == 1 ? "gemm-schur" : (kind == 2 ? "gemm-rot" : "gemm-panel"));
-            if (timed) CK(cudaEventRecord(next_event(), st_));
             if (st_acc_) {
                 st_acc_->launches++;
                 st_acc_->gemm_flops_exec += b.flops;
@@ -480,6 +488,18 @@ private:
         ev_marks_.push_back({(int)ev_used_, (double)kind});
         return next_event();
     }
+    // kinds: 0 panel GEMMs, 1 Schur GEMM, 2 rotation/merge GEMMs, 3 BK, 4 panel solve,
+    //        5 copies, 6 QR (pqr + form)
+    struct Timed {
+        Wave *w;
+        bool on;
+        Timed(Wave *w_, int kind) : w(w_), on(w_->time_kernels_) {
+            if (on) CK(cudaEventRecord(w->mark(kind), w->st_));
+        }
+        ~Timed() {
+            if (on) cudaEventRecord(w->next_event(), w->st_);
+        }
+    };
 
     // C (ra x cb) = Qa^T A Qb, Q == nullptr means identity (exact copy)
     void congruence(const double *A, int ra, int cb, const double *Qa, const double *Qb,
@@ -574,7 +594,10 @@ private:
         for (auto &mk : ev_marks_) {
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, ev_pool_[mk.first], ev_pool_[mk.first + 1]));
-            if (mk.second == 1) acc.ms_schur += ms;
+            const int kd = (int)mk.second;
+            if (kd >= 0 && kd < 8) acc.ms_kind[kd] += ms;
+            if (kd == 1) acc.ms_schur += ms;
+            if (kd == 3) acc.ms_bk += ms;
         }
         std::memcpy(counts, hc.data(), sizeof(int64_t) * 3 * s);
         for (int z = 0; z < s; ++z) status[z] = hs[z] ? H2L_SHIFT_SINGULAR : H2L_SHIFT_OK;
@@ -728,19 +751,100 @@ private:
                 }
             }
             flush(cb);
-            const int64_t vs = pad4(nR), cs = pad4(c);
-            double *tau, *norms;
-            int *piv, *used;
-            CK(cudaMallocFromPoolAsync((void **)&tau, sizeof(double) * vs * s_, pool_, st_));
-            CK(cudaMallocFromPoolAsync((void **)&piv, sizeof(int) * vs * s_, pool_, st_));
-            CK(cudaMallocFromPoolAsync((void **)&used, sizeof(int) * cs * s_, pool_, st_));
-            CK(cudaMallocFromPoolAsync((void **)&norms, sizeof(double) * cs * s_, pool_, st_));
-            int *d_active;
+            // ---- rank reveal: order the directions by a column-pivoted QR of the
+            // Gram matrix M = G G^T = U S^2 U^T (its columns are G's columns weighted
+            // toward the dominant singular directions), then take the rank from the
+            // exact energies of D = Q^T G (k_rrqr.cu)
+            Blk M = alloc(nR, nR, false), QT = alloc(nR, nR, false), DT = alloc(c, nR, false);
+            const int64_t ts = pad4(nR);
+            const int64_t pn = tail_rank_part_doubles(c, nR);
+            double *tau, *part, *norms;
+            int *piv, *used, *d_active;
+            CK(cudaMallocFromPoolAsync((void **)&tau, sizeof(double) * ts * s_, pool_, st_));
+            CK(cudaMallocFromPoolAsync((void **)&norms, sizeof(double) * ts * s_, pool_, st_));
+            CK(cudaMallocFromPoolAsync((void **)&piv, sizeof(int) * ts * s_, pool_, st_));
+            CK(cudaMallocFromPoolAsync((void **)&used, sizeof(int) * ts * s_, pool_, st_));
+            CK(cudaMallocFromPoolAsync((void **)&part, sizeof(double) * pn * s_, pool_, st_));
             CK(cudaMallocFromPoolAsync((void **)&d_active, sizeof(int) * s_, pool_, st_));
             activity_from_status(d_active);
-            CK(launch_pqr(GT.p, GT.bs, c, nR, nR, tau, piv, used, norms, vs, cs, d_tol_, d_rank_,
-                          d_dropped_, d_active, -1, s_, st_));
-            st_acc_->launches += 2;
+            {
+                GemmBatch g;  // M = G G^T = GT^T GT
+                add_gemm(g, gm(GT.p, GT.bs, nR, 1, GT.p, GT.bs, nR, 0, M.p, M.bs, nR, nR, nR, c,
+                               1.0, 0.0), s_);
+                flush(g, s_, 6);
+            }
+            {
+                Timed tm(this, 6);
+                // M is symmetric: its row-major storage is also its "columns as rows" layout
+                CK(launch_pqr(M.p, M.bs, nR, nR, nR, tau, piv, used, norms, ts, ts, d_tol_, d_rank_,
+                              d_dropped_, d_active, -2, s_, st_));
+                // all nR reflectors; with t = nR form_tr's row map is the identity (QT = Q^T)
+                CK(launch_form_tr(M.p, M.bs, nR, tau, piv, ts, nR, nR, QT.p, QT.bs, d_active, s_,
+                                  st_));
+            }
+            {
+                GemmBatch g;  // D^T = GT Q  (Q[k][n] = QT[n][k])
+                add_gemm(g, gm(GT.p, GT.bs, nR, 0, QT.p, QT.bs, nR, 1, DT.p, DT.bs, nR, c, nR, nR,
+                               1.0, 0.0), s_);
+                flush(g, s_, 6);
+            }
+            int *d_r1;
+            CK(cudaMallocFromPoolAsync((void **)&d_r1, sizeof(int) * s_, pool_, st_));
+            {
+                Timed tm(this, 6);
+                CK(launch_tail_rank(DT.p, DT.bs, c, nR, part, d_tol_, d_rank_, d_dropped_, d_r1,
+                                    d_active, s_, st_));
+            }
+            // deflation pass: the Gram matrix only orders directions whose energy is above
+            // ~1e-16 of the largest; re-order the rest from their own Gram matrix
+            {
+                std::vector<int> r1v(s_), a1(s_);
+                CK(cudaMemcpyAsync(r1v.data(), d_r1, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
+                CK(cudaMemcpyAsync(a1.data(), d_active, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
+                sync();
+                int r1 = nR;
+                for (int z = 0; z < s_; ++z)
+                    if (a1[z]) r1 = std::min(r1, r1v[z]);
+                const int nT = nR - r1;
+                if (nT > 1) {
+                    Blk M2 = alloc(nT, nT, false), Q2T = alloc(nT, nT, false);
+                    Blk DT2 = alloc(c, nT, false), QT2 = alloc(nT, nR, false);
+                    {
+                        GemmBatch g;  // M2 = D_tail D_tail^T (columns r1.. of DT)
+                        add_gemm(g, gm(DT.p + r1, DT.bs, nR, 1, DT.p + r1, DT.bs, nR, 0, M2.p,
+                                       M2.bs, nT, nT, nT, c, 1.0, 0.0), s_);
+                        flush(g, s_, 6);
+                    }
+                    {
+                        Timed tm(this, 6);
+                        CK(launch_pqr(M2.p, M2.bs, nT, nT, nT, tau, piv, used, norms, ts, ts, d_tol_,
+                                      d_rank_, d_dropped_, d_active, -2, s_, st_));
+                        CK(launch_form_tr(M2.p, M2.bs, nT, tau, piv, ts, nT, nT, Q2T.p, Q2T.bs,
+                                          d_active, s_, st_));
+                    }
+                    {
+                        GemmBatch g;  // DT2 = D_tail^T Q2 ; QT2 = Q2^T QT[r1:, :]
+                        add_gemm(g, gm(DT.p + r1, DT.bs, nR, 0, Q2T.p, Q2T.bs, nT, 1, DT2.p, DT2.bs,
+                                       nT, c, nT, nT, 1.0, 0.0), s_);
+                        add_gemm(g, gm(Q2T.p, Q2T.bs, nT, 0, QT.at(r1, 0), QT.bs, nR, 0, QT2.p,
+                                       QT2.bs, nR, nT, nR, nT, 1.0, 0.0), s_);
+                        flush(g, s_, 6);
+                    }
+                    CopyBatch cc;
+                    add_copy(cc, cp(DT2.p, DT2.bs, nT, DT.p + r1, DT.bs, nR, c, nT));
+                    add_copy(cc, cp(QT2.p, QT2.bs, nR, QT.at(r1, 0), QT.bs, nR, nT, nR));
+                    flush(cc);
+                    {
+                        Timed tm(this, 6);
+                        CK(launch_tail_rank(DT.p, DT.bs, c, nR, part, d_tol_, d_rank_, d_dropped_,
+                                            nullptr, d_active, s_, st_));
+                    }
+                    for (Blk *b : {&M2, &Q2T, &DT2, &QT2}) release(*b);
+                    st_acc_->launches += 8;
+                }
+            }
+            CK(cudaFreeAsync(d_r1, st_));
+            st_acc_->launches += 5;
             std::vector<int> rk(s_), act(s_);
             std::vector<double> dr(s_);
             CK(cudaMemcpyAsync(rk.data(), d_rank_, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
@@ -759,22 +863,22 @@ private:
                 st_acc_->flops += (2.0 * a * b * b - 2.0 / 3.0 * b * b * b) * s_;
             }
             if (t > 0) {
-                CK(launch_pqr(GT.p, GT.bs, c, nR, nR, tau, piv, used, norms, vs, cs, d_tol_, d_rank_,
-                              d_dropped_, d_active, t, s_, st_));
+                // Tr = [U_r^T ; U_s^T] = QT rows [t, nR) then [0, t)
                 Blk Tr = alloc(nR, nR, false);
-                CK(launch_form_tr(GT.p, GT.bs, nR, tau, piv, vs, nR, t, Tr.p, Tr.bs, d_active, s_, st_));
-                st_acc_->launches += 2;
+                CopyBatch rc;
+                add_copy(rc, cp(QT.at(t, 0), QT.bs, nR, Tr.p, Tr.bs, nR, nR - t, nR));
+                add_copy(rc, cp(QT.p, QT.bs, nR, Tr.at(nR - t, 0), Tr.bs, nR, t, nR));
+                flush(rc);
                 apply_rotation(i, Tr, t);
                 release(Tr);
                 ci.nR = nR - t;
                 ci.nS += t;
                 st_acc_->rank_added += t;
             }
-            CK(cudaFreeAsync(tau, st_));
-            CK(cudaFreeAsync(piv, st_));
-            CK(cudaFreeAsync(used, st_));
-            CK(cudaFreeAsync(norms, st_));
-            CK(cudaFreeAsync(d_active, st_));
+            for (void *q : {(void *)tau, (void *)norms, (void *)piv, (void *)used, (void *)part,
+                            (void *)d_active})
+                CK(cudaFreeAsync(q, st_));
+            for (Blk *b : {&M, &QT, &DT}) release(*b);
             release(GT);
         }
         // discard what is left in the redundant rows of i's fills (gldl.py:341-347)
@@ -898,8 +1002,11 @@ private:
                 tiles.push_back(t);
             }
             const PanelTile *dt = (const PanelTile *)stage(tiles.data(), sizeof(PanelTile) * tiles.size());
-            CK(launch_panel(dt, (int)tiles.size(), s_, D.p, D.bs, m, nR, perm, dinfo, ps, WI.p, XI.p,
-                            WI.bs, nR, st_));
+            {
+                Timed tm(this, 4);
+                CK(launch_panel(dt, (int)tiles.size(), s_, D.p, D.bs, m, nR, perm, dinfo, ps, WI.p,
+                                XI.p, WI.bs, nR, st_));
+            }
             dbg_sync("panel");
             st_acc_->launches++;
             GemmBatch g0;
@@ -996,7 +1103,10 @@ private:
         const int64_t scr = bk_scratch_doubles(n);
         double *scratch = nullptr;
         if (scr) CK(cudaMallocFromPoolAsync((void **)&scratch, sizeof(double) * scr * s_, pool_, st_));
-        CK(launch_bk_engine(dj, 1, s_, n, d_counts_, d_status_, scratch, scr, st_));
+        {
+            Timed tm(this, 3);
+            CK(launch_bk_engine(dj, 1, s_, n, d_counts_, d_status_, scratch, scr, st_));
+        }
         dbg_sync("bk");
         st_acc_->launches++;
         if (scratch) CK(cudaFreeAsync(scratch, st_));
@@ -1266,6 +1376,7 @@ static void merge_stats(h2l_stats &a, const h2l_stats &b) {
     a.launches += b.launches;
     a.schur_flops += b.schur_flops;
     a.gemm_flops_exec += b.gemm_flops_exec;
+    for (int k = 0; k < 8; ++k) a.ms_kind[k] += b.ms_kind[k];
 }
 
 class Engine {
@@ -1295,6 +1406,7 @@ public:
     }
     void inertia(const double *mu, int s, int64_t *counts, int32_t *status, h2l_stats *stats) {
         CK(cudaSetDevice(dev_));
+        const auto host0 = std::chrono::steady_clock::now();
         const int mb = waves_[0]->max_batch();
         const int nw = (s + mb - 1) / mb;
         const int C = std::min(concurrency_, nw);
@@ -1350,6 +1462,7 @@ public:
         h2l_stats tot{};
         for (auto &a : acc) merge_stats(tot, a);
         tot.ms_total = ms;
+        tot.ms_host = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host0).count();
         if (stats) *stats = tot;
     }
 

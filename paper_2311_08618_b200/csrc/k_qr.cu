@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(QR_THREADS) pqr_kernel(QrArgs a) {
     __shared__ double s_beta, s_tau, s_scale;
     const int z = blockIdx.x;
     if (a.active && !a.active[z]) {
-        if (threadIdx.x == 0 && a.target < 0) { a.rank[z] = 0; a.dropped[z] = 0.0; }
+        if (threadIdx.x == 0 && a.target == -1) { a.rank[z] = 0; a.dropped[z] = 0.0; }
         return;
     }
     double *GT = a.GT + z * a.gstride;
@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(QR_THREADS) pqr_kernel(QrArgs a) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
     const int c = a.c, nR = a.nR, kmax = min(c, nR);
     int j;
+    const bool full = a.target == -2;  // init and run to min(c, nR) steps (no tolerance)
     if (a.target < 0) {
         j = 0;
         for (int q = warp; q < c; q += nwarp) {
@@ -131,7 +132,9 @@ __global__ void __launch_bounds__(QR_THREADS) pqr_kernel(QrArgs a) {
         for (int q = threadIdx.x; q < c; q += blockDim.x)
             if (!used[q]) part += norms[q];
         tail = sqrt(block_sum(part, redv));
-        if (a.target < 0) {
+        if (full) {
+            // no early stop
+        } else if (a.target < 0) {
             if (tail <= a.tol[z]) break;
         } else if (j >= a.target) {
             break;
@@ -184,7 +187,7 @@ __global__ void __launch_bounds__(QR_THREADS) pqr_kernel(QrArgs a) {
         __syncthreads();
         ++j;
     }
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && !full) {
         a.rank[z] = j;
         if (a.target < 0) a.dropped[z] = tail;
     }
