@@ -106,6 +106,7 @@ typedef struct h2l_stats {
                              1 Schur GEMM, 2 rotation/merge GEMMs, 3 BK, 4 panel solve,
                              5 copies, 6 recompression QR, 7 unused */
     double ms_host;       /* wall-clock ms of the call on the host */
+    double mem_peak;      /* bytes: high-water mark of the waves' device pools during the call */
 } h2l_stats;
 
 int h2l_create(h2l_engine **engine, int device);

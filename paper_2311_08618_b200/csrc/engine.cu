@@ -122,6 +122,16 @@ public:
         cudaMemPoolDestroy(pool_);
     }
 
+    // pool high-water mark (reset at the start of each call)
+    void reset_mem_high() {
+        uint64_t z = 0;
+        CK(cudaMemPoolSetAttribute(pool_, cudaMemPoolAttrReservedMemHigh, &z));
+    }
+    double mem_high() {
+        uint64_t v = 0;
+        CK(cudaMemPoolGetAttribute(pool_, cudaMemPoolAttrReservedMemHigh, &v));
+        return (double)v;
+    }
     void set_option(const std::string &k, int64_t v) {
         if (k == "max_batch") max_batch_ = (int)std::max<int64_t>(1, v);
         else if (k == "time_kernels") time_kernels_ = v != 0;
@@ -1082,16 +1092,40 @@ private:
             release(Xb);
         }
         st_acc_->flops += flops * s_;
-        // ---- retire the redundant rows / columns of i (gldl.py:411-417)
-        CopyBatch zc;
-        add_copy(zc, zero(D.p, D.bs, m, nR, m));
-        add_copy(zc, zero(D.at(nR, 0), D.bs, m, m - nR, nR));
-        for (auto &k : adj_off_[i]) {
-            Blk &O = offd_.at(k);
-            if (k.first == i) add_copy(zc, zero(O.p, O.bs, O.cols, nR, O.cols));
-            else add_copy(zc, zero(O.p, O.bs, O.cols, O.rows, nR));
+        // ---- retire the redundant rows / columns of i (gldl.py:411-417).  The
+        // reference zeroes them; here every block of i is compacted to its skeleton
+        // rows / columns (the R part is zero from now on and never read again), and i
+        // becomes an m = nS, nR = 0 cluster: later panels, Schur targets, merges and
+        // fill blocks see only live rows, and the front's memory shrinks as it moves.
+        {
+            CopyBatch zc;
+            std::vector<std::pair<Blk *, Blk>> repl;
+            Blk nd = alloc(nS, nS, false);
+            add_copy(zc, cp(D.at(nR, nR), D.bs, m, nd.p, nd.bs, nS, nS, nS));
+            repl.push_back({&D, nd});
+            for (auto *store : {&offd_, &fill_}) {
+                auto &adj = (store == &offd_) ? adj_off_[i] : adj_fill_[i];
+                for (auto &k : adj) {
+                    Blk &O = store->at(k);
+                    Blk N;
+                    if (k.first == i) {
+                        N = alloc(nS, O.cols, false);
+                        add_copy(zc, cp(O.at(nR, 0), O.bs, O.cols, N.p, N.bs, N.cols, nS, O.cols));
+                    } else {
+                        N = alloc(O.rows, nS, false);
+                        add_copy(zc, cp(O.at(0, nR), O.bs, O.cols, N.p, N.bs, N.cols, O.rows, nS));
+                    }
+                    repl.push_back({&O, N});
+                }
+            }
+            flush(zc);
+            for (auto &r : repl) {
+                release(*r.first);
+                *r.first = r.second;
+            }
+            ci.m = nS;
+            ci.nR = 0;
         }
-        flush(zc);
         CK(cudaFreeAsync(perm, st_));
         CK(cudaFreeAsync(dinfo, st_));
         elim_[i] = 1;
@@ -1416,6 +1450,7 @@ public:
         }
         std::vector<h2l_stats> acc(C);
         for (auto &a : acc) a = h2l_stats{};
+        for (int t = 0; t < C; ++t) waves_[t]->reset_mem_high();
         cudaStream_t s0 = waves_[0]->stream();
         CK(cudaEventRecord(ev_[0], s0));
         for (int t = 1; t < C; ++t) CK(cudaStreamWaitEvent(waves_[t]->stream(), ev_[0], 0));
@@ -1462,6 +1497,7 @@ public:
         h2l_stats tot{};
         for (auto &a : acc) merge_stats(tot, a);
         tot.ms_total = ms;
+        for (int t = 0; t < C; ++t) tot.mem_peak += waves_[t]->mem_high();
         tot.ms_host = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host0).count();
         if (stats) *stats = tot;
     }

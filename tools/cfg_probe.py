@@ -20,7 +20,8 @@ print(f"{name} n={cloud.n} depth={L} build {t1 - t0:.1f}s arena {Hd._arena.numel
       f"max rank all {Hd.max_rank()}", flush=True)
 eng = _native.engine_for(Hd, 0)
 eng.set_option("max_batch", mb)
-eng.set_option("time_kernels", 1)
+eng.set_option("time_kernels", int(os.environ.get("TK", "1")))
+eng.set_option("concurrency", int(os.environ.get("C", "2")))
 t2 = time.perf_counter()
 eng_t = time.perf_counter() - t2
 for rep in range(int(os.environ.get("REPS", "1"))):
@@ -32,4 +33,5 @@ for rep in range(int(os.environ.get("REPS", "1"))):
     print({k: (round(v, 3) if isinstance(v, float) else v) for k, v in st.items()}, flush=True)
 print("schur TF/s", st["schur_flops"] / (st["ms_schur"] / 1e3) / 1e12 if st["ms_schur"] else None,
       "alg TF/s", st["flops"] / (st["ms_total"] / 1e3) / 1e12, flush=True)
-print("mem peak GB", torch.cuda.max_memory_allocated() / 1e9)
+print("mem peak GB", torch.cuda.max_memory_allocated() / 1e9, "device free/total GB",
+      [v / 1e9 for v in torch.cuda.mem_get_info()])
