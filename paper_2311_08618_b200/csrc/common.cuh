@@ -100,7 +100,7 @@ void launch_copy_prefixed(const CopyTask *dev_tasks, const int *dev_prefix, int 
 
 int gemm_tiles(int M, int N);
 void launch_gemm(const GemmTask *dev_tasks, const int *dev_tile_prefix, int ntasks,
-                 int total_tiles, int nshift, cudaStream_t st);
+                 int total_tiles, int nshift, cudaStream_t st, bool schur = false);
 
 int64_t bk_scratch_doubles(int n);
 cudaError_t launch_bk_engine(const BkJob *dev_jobs, int njobs, int nshift, int nmax,

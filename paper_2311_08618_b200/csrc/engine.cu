@@ -286,7 +286,8 @@ private:
     int *d_status_ = nullptr, *d_rank_ = nullptr;
     std::vector<Cl> cl_;
     std::vector<Blk> diag_;
-    std::vector<char> elim_;
+    std::vector<char> elim_, pend_diag_;
+    std::set<Pair> pend_off_;
     std::map<Pair, Blk> offd_, coup_, fill_;
     std::vector<std::set<Pair>> adj_off_, adj_fill_, adj_coup_;
     h2l_stats *st_acc_ = nullptr;
@@ -331,6 +332,47 @@ private:
         CK(cudaMemcpyAsync(d, h, nbytes, cudaMemcpyHostToDevice, st_));
         stage_.off += bytes;
         return d;
+    }
+    // H2L_GEMMSTATS: flop-weighted histogram of Schur GEMM shapes (printed per wave)
+    std::map<std::string, double> ghist_;
+    static bool gemmstats_on() {
+        static const bool on = getenv("H2L_GEMMSTATS") != nullptr;
+        return on;
+    }
+    template <class GB>
+    void gemm_hist(const GB &b) {
+        if (!gemmstats_on()) return;
+        auto bucket = [](int v) { int q = 16; while (q < v) q *= 2; return q; };
+        for (auto &t : b.t) {
+            char key[64];
+            snprintf(key, sizeof key, "M<=%d N<=%d K<=%d", bucket(t.M), bucket(t.N), bucket(t.K));
+            ghist_[key] += 2.0 * t.M * t.N * (double)t.K * s_;
+        }
+        ghist_["#launch tiles"] += b.tiles;
+        ghist_["#launches"] += 1;
+    }
+    void gemm_hist_print() {
+        if (!gemmstats_on()) return;
+        std::vector<std::pair<double, std::string>> v;
+        double tot = 0;
+        for (auto &kv : ghist_) if (kv.first[0] != '#') { v.push_back({kv.second, kv.first}); tot += kv.second; }
+        std::sort(v.rbegin(), v.rend());
+        fprintf(stderr, "schur gemm: %.3g flops, %.0f launches, %.0f tiles (per shift-row)\n", tot,
+                ghist_["#launches"], ghist_["#launch tiles"]);
+        for (size_t q = 0; q < v.size() && q < 25; ++q)
+            fprintf(stderr, "  %-28s %5.1f%%\n", v[q].second.c_str(), 100.0 * v[q].first / tot);
+        ghist_.clear();
+    }
+    // H2L_MEMTRACE: pool usage (current / high-water) at level boundaries
+    void memtrace(const char *what, int level) {
+        static const bool on = getenv("H2L_MEMTRACE") != nullptr;
+        if (!on) return;
+        CK(cudaStreamSynchronize(st_));
+        uint64_t cur = 0, hi = 0;
+        CK(cudaMemPoolGetAttribute(pool_, cudaMemPoolAttrUsedMemCurrent, &cur));
+        CK(cudaMemPoolGetAttribute(pool_, cudaMemPoolAttrUsedMemHigh, &hi));
+        fprintf(stderr, "memtrace %s level %d: used %.2f GB high %.2f GB\n", what, level, cur / 1e9,
+                hi / 1e9);
     }
     void dbg_sync(const char *what = "") {
         if (guard_mode()) {
@@ -482,7 +524,8 @@ private:
             const int *dp = (const int *)stage(b.pre.data(), sizeof(int) * b.pre.size());
             {
                 Timed tm(this, kind);
-                launch_gemm(dt, dp, (int)b.t.size(), b.tiles, nshift, st_);
+                launch_gemm(dt, dp, (int)b.t.size(), b.tiles, nshift, st_, kind == 1);
+                if (kind == 1) gemm_hist(b);
             }
             CK(cudaGetLastError());
             dbg_sync(kind == 1 ? "gemm-schur" : (kind == 2 ? "gemm-rot" : "gemm-panel"));
@@ -579,6 +622,7 @@ private:
             Blk root;
             while (true) {
                 process_level(level);
+                memtrace("level done", level);
                 if (kind_ == H2L_FLAT) {
                     root = merge_flat();
                     break;
@@ -588,12 +632,14 @@ private:
                     break;
                 }
                 merge_pairwise(level, false);
+                memtrace("merged", level);
                 --level;
             }
             factor_root(root);
             release(root);
             clear_level();
         }
+        gemm_hist_print();
         // timings of Schur launches
         std::vector<int64_t> hc(3 * s);
         std::vector<int> hs(s);
@@ -653,42 +699,89 @@ private:
         }
     }
 
+    // Leaf blocks are materialised lazily (just before the first elimination that
+    // touches them) from the shift-independent skeleton blocks: together with the
+    // compaction of eliminated clusters only the moving front is held per shift.
     void assemble_leaf() {
         const int L = depth_, nl = 1 << L;
         clear_level();
         cl_.assign(nl, Cl{});
         diag_.assign(nl, Blk{});
         reset_adjacency(nl);
-        CopyBatch c;
+        pend_diag_.assign(nl, 0);
+        pend_off_.clear();
         for (int i = 0; i < nl; ++i) {
             const int m = lsize(i);
             if (m == 0) continue;
             const int r = std::max(0, brank_[node(L, i)]);
             cl_[i] = Cl{m, m - r, r, r};
-            diag_[i] = alloc(m, m, false);
-            CopyTask t = cp(skel_diag_[i], 0, m, diag_[i].p, diag_[i].bs, m, m, m);
-            t.shift_diag = 1;
-            add_copy(c, t);
+            pend_diag_[i] = 1;
         }
         for (auto &pr : dense_) {
-            const int i = pr.first, j = pr.second;
-            Blk b = alloc(lsize(i), lsize(j), false);
-            add_copy(c, cp(skel_off_.at(pr), 0, b.cols, b.p, b.bs, b.cols, b.rows, b.cols));
-            offd_[pr] = b;
-            adj_off_[i].insert(pr);
-            adj_off_[j].insert(pr);
+            offd_[pr] = Blk{};
+            pend_off_.insert(pr);
+            adj_off_[pr.first].insert(pr);
+            adj_off_[pr.second].insert(pr);
         }
+        CopyBatch c;
         load_couplings(L, c);
+        flush(c);
+    }
+    void ensure_diag(int i, CopyBatch &c) {
+        if (i >= (int)pend_diag_.size() || !pend_diag_[i]) return;
+        pend_diag_[i] = 0;
+        const int m = lsize(i);
+        diag_[i] = alloc(m, m, false);
+        CopyTask t = cp(skel_diag_[i], 0, m, diag_[i].p, diag_[i].bs, m, m, m);
+        t.shift_diag = 1;
+        add_copy(c, t);
+    }
+    void ensure_off(const Pair &pr, CopyBatch &c) {
+        auto it = pend_off_.find(pr);
+        if (it == pend_off_.end()) return;
+        pend_off_.erase(it);
+        Blk b = alloc(lsize(pr.first), lsize(pr.second), false);
+        add_copy(c, cp(skel_off_.at(pr), 0, b.cols, b.p, b.bs, b.cols, b.rows, b.cols));
+        offd_[pr] = b;
+    }
+    // every block the recompression and elimination of i can touch
+    void ensure_front(int i) {
+        if (pend_off_.empty() && !std::count(pend_diag_.begin(), pend_diag_.end(), 1)) return;
+        CopyBatch c;
+        ensure_diag(i, c);
+        std::vector<int> partners;
+        for (auto &k : adj_off_[i]) {
+            partners.push_back(k.first == i ? k.second : k.first);
+            ensure_off(k, c);
+        }
+        std::sort(partners.begin(), partners.end());
+        for (size_t x = 0; x < partners.size(); ++x) {
+            ensure_diag(partners[x], c);
+            if (!pend_off_.empty())
+                for (size_t y = x + 1; y < partners.size(); ++y)
+                    ensure_off({partners[x], partners[y]}, c);
+        }
+        flush(c, d_mu_);
+    }
+    void ensure_all() {
+        CopyBatch c;
+        for (int i = 0; i < (int)pend_diag_.size(); ++i) ensure_diag(i, c);
+        std::vector<Pair> rest(pend_off_.begin(), pend_off_.end());
+        for (auto &pr : rest) ensure_off(pr, c);
         flush(c, d_mu_);
     }
 
     void process_level(int level) {
         const int nc = 1 << level;
+        const bool leaf = level == depth_;
         for (int i = 0; i < nc; ++i) {
             if (cl_[i].m == 0) continue;
+            if (leaf) ensure_front(i);
             recompress(i);
             eliminate(i);
+            if ((i & (nc / 8 - 1)) == 0 && nc >= 8) memtrace("cluster", i);
         }
+        if (leaf) ensure_all();
         // fold fills of this level's low-rank pairs into the couplings (gldl.py:284-294)
         auto it = lowrank_.find(level);
         if (it != lowrank_.end()) {

@@ -28,7 +28,6 @@ namespace h2l {
 
 namespace {
 
-constexpr int BK = 16, SK = BK + 4;
 
 __device__ __forceinline__ int find_task(const int *prefix, int ntasks, int tile) {
     int lo = 0, hi = ntasks - 1;
@@ -54,9 +53,11 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_, bool CSTAGE_ = true, int MINB_ = 1>
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, bool CSTAGE_ = true, int MINB_ = 1,
+          int BK_ = 16>
 struct GemmCfg {
     static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_;
+    static constexpr int BK = BK_, SK = BK_ + 4;  // K chunk; padded shared row (conflict-free)
     static constexpr bool CSTAGE = CSTAGE_;  // prefetch C into shared memory
     static constexpr int MINB = MINB_;       // min resident CTAs per SM (register cap)
     static constexpr int WARPS = (BM / WM) * (BN / WN);
@@ -67,35 +68,56 @@ struct GemmCfg {
         sizeof(double) * ((size_t)STAGES * (BM + BN) * SK + (CSTAGE ? (size_t)BM * CS : 0));
 };
 
-// Stage the ROWS x 16 chunk of op(X) starting at (row0, k0) into S[ROWS][SK].
-// op: element (r, k) = trans ? X[k*ld + r] : X[r*ld + k]
-template <int ROWS, int THREADS>
-__device__ __forceinline__ void load_chunk(double (*S)[SK], const double *X, int ld, int trans,
-                                           int rows, int K, int row0, int k0, int tid) {
-    constexpr int TOTAL = ROWS * BK;
-    if (!trans) {
-#pragma unroll
-        for (int e = tid; e < TOTAL; e += THREADS) {
-            const int rl = e >> 4, kl = e & 15;
-            const int r = row0 + rl, k = k0 + kl;
-            const bool ok = r < rows && k < K;
-            cp_async8(&S[rl][kl], ok ? X + (int64_t)r * ld + k : X, ok);
+// Per-thread staging plan of the ROWS x 16 chunks of op(X), element (r, k) =
+// trans ? X[k*ld + r] : X[r*ld + k].  Thread tid copies the elements
+// e = tid + q*THREADS (q < ROWS*16/THREADS) of every chunk; their global and
+// shared addresses differ by fixed strides, so the pointers, row predicates
+// and shared offsets are computed once per tile and each chunk costs one add.
+template <int ROWS, int THREADS, int BK, int SK>
+struct Loader {
+    static_assert(THREADS % ROWS == 0 && THREADS % BK == 0, "loader layout");
+    static constexpr int NQ = ROWS * BK / THREADS;
+    const double *p;        // element q = 0 of chunk 0
+    int64_t dq, dk;         // pointer strides per q and per chunk (doubles)
+    unsigned soff, sdq;     // shared byte offset of q = 0 and per-q stride
+    unsigned rowok;         // bit q: row in range
+    int kl0, kstep;         // k within the chunk of element q: kl0 + q * kstep
+    __device__ __forceinline__ Loader(const double *X, int ld, int trans, int rows, int row0,
+                                      int tid) {
+        int rl0, rstep;
+        if (!trans) {  // rows contiguous in k: consecutive threads walk k
+            rl0 = tid / BK; rstep = THREADS / BK; kl0 = tid % BK; kstep = 0;
+            p = X + (int64_t)(row0 + rl0) * ld + kl0;
+            dq = (int64_t)rstep * ld; dk = BK;
+        } else {       // columns contiguous in r: consecutive threads walk r
+            rl0 = tid % ROWS; rstep = 0; kl0 = tid / ROWS; kstep = THREADS / ROWS;
+            p = X + (int64_t)kl0 * ld + row0 + rl0;
+            dq = (int64_t)kstep * ld; dk = (int64_t)BK * ld;
         }
-    } else {
+        soff = (unsigned)((rl0 * SK + kl0) * sizeof(double));
+        sdq = (unsigned)((rstep * SK + kstep) * sizeof(double));
+        rowok = 0;
 #pragma unroll
-        for (int e = tid; e < TOTAL; e += THREADS) {
-            const int rl = e % ROWS, kl = e / ROWS;
-            const int r = row0 + rl, k = k0 + kl;
-            const bool ok = r < rows && k < K;
-            cp_async8(&S[rl][kl], ok ? X + (int64_t)k * ld + r : X, ok);
+        for (int q = 0; q < NQ; ++q) rowok |= (row0 + rl0 + q * rstep < rows) ? (1u << q) : 0u;
+    }
+    // stage chunk c (k0 = c*BK) into the shared buffer at byte address sbase
+    __device__ __forceinline__ void load(unsigned sbase, int c, int K) const {
+        const double *pc = p + c * dk;
+        const int krem = K - c * BK;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const bool ok = ((rowok >> q) & 1u) && (kl0 + q * kstep < krem);
+            // src-size 0 (zero fill) reads nothing, so the address needs no clamp
+            asm volatile("cp.async.ca.shared.global.L2::128B [%0], [%1], 8, %2;\n"
+                         ::"r"(sbase + soff + q * sdq), "l"(pc + q * dq), "r"(ok ? 8 : 0));
         }
     }
-}
+};
 
 template <class Cfg>
-__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_kernel(const GemmTask *tasks,
-                                                            const int *prefix, int ntasks) {
+__device__ __forceinline__ void gemm_body(const GemmTask *tasks, const int *prefix, int ntasks) {
     constexpr int BM = Cfg::BM, BN = Cfg::BN, STAGES = Cfg::STAGES, FM = Cfg::FM, FN = Cfg::FN;
+    constexpr int BK = Cfg::BK, SK = Cfg::SK;
     constexpr int THREADS = Cfg::THREADS, CS = Cfg::CS;
     extern __shared__ __align__(16) double gsm[];
     double (*As)[BM][SK] = reinterpret_cast<double (*)[BM][SK]>(gsm);
@@ -138,11 +160,16 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_kernel(const Gem
         for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     const int nk = (tk.K + BK - 1) / BK;
+    const Loader<BM, THREADS, BK, SK> la(A, tk.lda, tk.tA, tk.M, m0, tid);
+    const Loader<BN, THREADS, BK, SK> lb(B, tk.ldb, b_trans, tk.N, n0, tid);
+    const unsigned sA = (unsigned)__cvta_generic_to_shared(&As[0][0][0]);
+    const unsigned sB = (unsigned)__cvta_generic_to_shared(&Bs[0][0][0]);
+    constexpr unsigned SA_STAGE = BM * SK * sizeof(double), SB_STAGE = BN * SK * sizeof(double);
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
         if (s < nk) {
-            load_chunk<BM, THREADS>(As[s], A, tk.lda, tk.tA, tk.M, tk.K, m0, s * BK, tid);
-            load_chunk<BN, THREADS>(Bs[s], B, tk.ldb, b_trans, tk.N, tk.K, n0, s * BK, tid);
+            la.load(sA + s * SA_STAGE, s, tk.K);
+            lb.load(sB + s * SB_STAGE, s, tk.K);
         }
         cp_commit();
     }
@@ -152,8 +179,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_kernel(const Gem
         const int nxt = kc + STAGES - 1;
         if (nxt < nk) {
             const int sl = nxt % STAGES;
-            load_chunk<BM, THREADS>(As[sl], A, tk.lda, tk.tA, tk.M, tk.K, m0, nxt * BK, tid);
-            load_chunk<BN, THREADS>(Bs[sl], B, tk.ldb, b_trans, tk.N, tk.K, n0, nxt * BK, tid);
+            la.load(sA + sl * SA_STAGE, nxt, tk.K);
+            lb.load(sB + sl * SB_STAGE, nxt, tk.K);
         }
         cp_commit();
         const int cur = kc % STAGES;
@@ -215,6 +242,18 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_kernel(const Gem
     }
 }
 
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_kernel(const GemmTask *tasks,
+                                                            const int *prefix, int ntasks) {
+    gemm_body<Cfg>(tasks, prefix, ntasks);
+}
+// same code under its own name so profiles separate the Schur updates (K6)
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) schur_gemm_kernel(const GemmTask *tasks,
+                                                                  const int *prefix, int ntasks) {
+    gemm_body<Cfg>(tasks, prefix, ntasks);
+}
+
 // production configuration (chosen with tools/gemm_bench.py)
 using Prod = GemmCfg<64, 64, 32, 32, 2, false, 4>;
 
@@ -234,8 +273,15 @@ int gemm_tiles(int M, int N) {
 }
 
 void launch_gemm(const GemmTask *dev_tasks, const int *dev_tile_prefix, int ntasks,
-                 int total_tiles, int nshift, cudaStream_t st) {
+                 int total_tiles, int nshift, cudaStream_t st, bool schur) {
     if (ntasks <= 0 || total_tiles <= 0 || nshift <= 0) return;
+    if (schur) {
+        smem_optin(schur_gemm_kernel<Prod>);
+        dim3 grid(total_tiles, nshift);
+        schur_gemm_kernel<Prod><<<grid, Prod::THREADS, Prod::SMEM, st>>>(dev_tasks, dev_tile_prefix,
+                                                                          ntasks);
+        return;
+    }
     launch_cfg<Prod>(dev_tasks, dev_tile_prefix, ntasks, total_tiles, nshift, st);
 }
 
@@ -248,7 +294,10 @@ using V4 = GemmCfg<64, 64, 32, 32, 2, false, 4>;
 using V5 = GemmCfg<128, 64, 32, 32, 2, false, 2>;
 using V6 = GemmCfg<64, 64, 32, 16, 2, false, 6>;
 using V7 = GemmCfg<128, 64, 32, 32, 3, false, 2>;
-#define H2L_VARIANTS(X) X(0, V0) X(1, V1) X(2, V2) X(3, V3) X(4, V4) X(5, V5) X(6, V6) X(7, V7)
+using V8 = GemmCfg<64, 64, 32, 32, 2, false, 3, 32>;
+using V9 = GemmCfg<64, 64, 32, 32, 3, false, 2, 32>;
+#define H2L_VARIANTS(X) \
+    X(0, V0) X(1, V1) X(2, V2) X(3, V3) X(4, V4) X(5, V5) X(6, V6) X(7, V7) X(8, V8) X(9, V9)
 
 int gemm_variant_tiles(int v, int M, int N) {
     if (M <= 0 || N <= 0) return 0;

@@ -16,9 +16,12 @@ f.argtypes = [ctypes.c_int] * 8 + [ctypes.POINTER(ctypes.c_double)] * 2
 f.restype = ctypes.c_int
 NAMES = ["64x64 w32x32 s3 Csm", "64x128 w32x64 s3 Csm", "64x64 w32x32 s2 min5",
          "64x64 w32x32 s3 min3", "64x64 w32x32 s2 min4", "128x64 w32x32 s2 min2",
-         "64x64 w32x16 s2 min6", "128x64 w32x32 s3 min2"]
+         "64x64 w32x16 s2 min6", "128x64 w32x32 s3 min2", "64x64 BK32 s2 min3",
+         "64x64 BK32 s3 min2"]
 shapes = [(128, 128, 128, 91, 256), (256, 256, 192, 60, 32), (64, 64, 64, 300, 64),
-          (128, 128, 128, 16, 8)]
+          (200, 200, 160, 400, 4), (256, 256, 32, 200, 4)]
+if len(sys.argv) > 1:
+    shapes = [tuple(int(v) for v in a.split(",")) for a in sys.argv[1:]]
 for (M, N, K, nt, ns) in shapes:
     for v in range(len(NAMES)):
         ms, md = ctypes.c_double(), ctypes.c_double()
