@@ -1,33 +1,52 @@
-"""Benchmark: H2-LDL inertia evaluations per second on B200 (BASELINE.json metric).
+"""Benchmark: H2-LDL inertia evaluations/s and s per k-th eigenvalue on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config cfg1] [--batch S]
+                    [--config cfg2|cfg1] [--batch S] [--eig]
 
-Workload (config.workload): BASELINE config 1 -- 3D 1/r kernel, n = 2048
-uniform points in [0,1]^3 (seed 0, Morton order), leaf 128, eta = 1,
-eps = 1e-8.  This is the only configuration whose input (the H2 matrix) can
-be built today (configs 2-5 need the GPU construction that SURVEY.md §8f
-lists next).  A step = one shift-batched sweep of the generalized LDL^T over
-S shifts (default 256) spread over the spectrum; `value` = shifts factorized
-per second over K timed steps (device time, CUDA events on the engine's
-stream, max over ranks); inputs (the uploaded H payload, 17.8 MB, and its
-s-batched working copies, 4.6 GB per step at S = 256) are resident in HBM and exceed L2,
-so no flush is needed.  `e2e` = the same metric through the public API
-`inertia_batch(H, mus)` with host shift lists and host counts (H2D of the
-shifts and D2H of the counts inside the timed region, wall clock).
+Workload (`config.workload`, BASELINE.json configs[1] = "cfg2" by default):
+3D 1/r kernel (A_ii = 0), n = 65,536 uniform points in [0,1]^3 (seed 0,
+Morton order), leaf 256, eta = 1, construction tolerance 1e-8, eps_ev = 1e-8.
+The H2 matrix is built on the device (gpu_build.construct_device, the
+reference's sampling algorithm) and the search interval comes from the
+Gershgorin row sums of the kernel matrix (gpu_build.gershgorin_device).
 
-Multi-GPU (torchrun): one rank per GPU, each with its own replica and S
-shifts per step (weak scaling; the path shards over shifts, no collective in
-the data path -- SURVEY.md §8e).
+A step is one batched sweep of the generalized LDL^T over the S shifts of one
+multisection round for k = n/2 (the shifts the eigenvalue search actually
+visits, starting from the Gershgorin interval: rounds 1..W are the warm-up,
+rounds W+1..W+K are timed).  `value` = shifts factorized per second over the K
+timed steps: device time (CUDA events on the engine stream around every
+h2l_inertia call), max over ranks.  The uploaded H (12.3 GB) and the per-shift
+working blocks (~16 GB per shift) are resident in HBM and exceed L2 by
+two orders of magnitude, so no flush is needed.  S defaults to 7 for cfg2: one
+3-level multisection round, the most shifts whose working set fits the GPU
+at once (BASELINE's "32 shifts per factorization" needs ~520 GB); `single_shift`
+reports the one-shift-per-step rate for comparison.
 
-`--impl reference`: the reference algorithm on the host CPU through the
-oracle port (oracle/engine_ref.py, the reference's engine restated in
-numpy/scipy with the reference kernel's C restatement), all host cores as
-worker processes, rank 0 only.
+`e2e` replays the K timed shift lists through the public API
+`inertia_batch(H, mus)` (host shifts in, host InertiaCount out, the engine's
+pinned H2D/D2H copies inside the timed region; wall clock).
+
+`eigenvalue`: seconds per k-th eigenvalue.  By default projected from the
+measured step times (rounds needed = ceil(log2(width/eps_ev) / 3)); with
+--eig the multisection search for k in {1, n/2, n} runs to completion.
+
+Multi-GPU (torchrun): one rank per GPU, each with a replica of H; a round has
+S x N shifts sharded over the ranks and one NCCL all-gather of the integer
+counts (multigpu.ShardedEvaluator) -- weak scaling in shifts per step.
+
+`cpu_baseline` / `--impl reference`: the reference algorithm on the host
+through the oracle port (oracle/engine_ref.py) on the same H (exported to
+host memory), BLAS threads = all host cores.  A cfg2 factorization takes
+about an hour on the CPU, so each sample is the first T seconds of one
+factorization: its elimination flops (survey §8d count, the oracle tallies
+them) divided by the flops of a whole factorization (`elim_flops` of the
+device run, or profiles/r1_cfg2_workload.json for the reference arm) scale
+the sample to evaluations/s.
 """
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -39,8 +58,10 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-METRIC = "H2-LDL inertia evals/s (cfg1 n=2048 3D 1/r leaf 128, shift-batched)"
+METRIC = "H2-LDL inertia evals/s and s per k-th eigenvalue (eps 1e-8), 1/2/4/8 B200"
 UNIT = "inertia evals/s"
+EPS_EV = 1e-8
+WORKLOAD_FILE = os.path.join(ROOT, "profiles", "r1_cfg2_workload.json")
 
 
 def _dist():
@@ -48,12 +69,6 @@ def _dist():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
-
-
-def shifts_for(eigs_lo, eigs_hi, s, step, rank):
-    """Deterministic shifts spread over [lo, hi] (distinct per step and rank)."""
-    rng = np.random.default_rng(1000 * step + rank)
-    return np.sort(rng.uniform(eigs_lo, eigs_hi, s))
 
 
 class ClockSampler:
@@ -79,7 +94,7 @@ class ClockSampler:
                     self.rows.append([v.strip() for v in out.split(",")])
             except Exception:  # noqa: BLE001
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.5)
 
     def start(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -119,99 +134,138 @@ def measure_fp64_peak(torch, dev):
     return 2.0 * n ** 3 / best / 1e12
 
 
-def build_cfg1():
+# ------------------------------------------------------------------ workloads
+class Workload:
+    name = ""
+    n = 0
+    k = 0
+    interval = (0.0, 0.0)
+    H = None
+    host_H = None
+    construct_s = None
+    config = {}
+    eigs = None        # exact spectrum when known (cfg1 golden)
+
+
+def workload_cfg2(device=True):
+    from paper_2311_08618_b200 import gpu_build
+
+    w = Workload()
+    w.name = "cfg2"
+    t0 = time.perf_counter()
+    w.H, cloud = gpu_build.config_device("cfg2")
+    import torch
+
+    torch.cuda.synchronize()
+    w.construct_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    w.interval = gpu_build.gershgorin_device(w.H._kernel)
+    w.interval_s = time.perf_counter() - t0
+    w.n = cloud.n
+    w.k = w.n // 2
+    w.config = {"workload": "cfg2", "n": w.n, "kernel": "1/r (A_ii = 0)",
+                "points": "uniform [0,1]^3 seed 0", "leaf": 256, "eta": 1.0, "eps": 1e-8,
+                "eps_ev": EPS_EV, "k": w.k, "interval": "Gershgorin row sums of A (device)"}
+    return w
+
+
+def workload_cfg1():
     from paper_2311_08618_b200 import configs, construct
 
-    cloud, kern, tree, st = configs.config_problem("cfg1", seed=0)
-    return construct(kern, tree, st, configs.CONFIGS["cfg1"].eps)
-
-
-def cfg1_interval():
-    z = np.load(os.path.join(ROOT, "tests", "golden", "cfg1.npz"))
-    return tuple(float(v) for v in z["interval"]), z["eigs"]
-
-
-# ------------------------------------------------------------------ reference
-def _ref_worker(args):
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    mus, = args
-    from oracle import engine_ref
-
-    H = build_cfg1()
-    cache = {}
-    out = []
-    for mu in mus:
-        out.append(engine_ref.inertia(H, float(mu), skel_cache=cache))
-    return out
-
-
-def run_reference(args):
-    world, rank, _ = _dist()
-    if rank != 0:
-        return
-    import multiprocessing as mp
-
-    # spawn (not fork): a forked child inherits the parent's OpenBLAS thread pool
-    # in a broken state and can deadlock on its first BLAS call
-    for var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
-        os.environ[var] = "1"
-    cores = os.cpu_count() or 1
-    (lo, hi), _ = cfg1_interval()
-    ctx = mp.get_context("spawn")
-    with ctx.Pool(cores) as pool:
-        # warm the per-process skeleton caches / imports
-        pool.map(_ref_worker, [([0.0],)] * cores)
-        per = 1  # shifts per worker per step: one factorization each (~0.5 s)
-        for w in range(args.warmup):
-            pool.map(_ref_worker, [(shifts_for(lo, hi, per, w, q),) for q in range(cores)])
-        t0 = time.perf_counter()
-        for k in range(args.steps):
-            pool.map(_ref_worker, [(shifts_for(lo, hi, per, 100 + k, q),) for q in range(cores)])
-        dt = time.perf_counter() - t0
-    total = cores * per * args.steps
-    v = total / dt
-    line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": "cfg1", "n": 2048, "leaf": 128,
-                                       "kernel": "1/r", "eps": 1e-8, "shifts_per_step": total // args.steps},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{cores} worker processes x {per} factorization per step "
-                                   f"(oracle/engine_ref.py, OPENBLAS_NUM_THREADS=1)"},
-        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-
-
-def cpu_baseline_sample(seconds=15.0):
-    """Oracle port on one host core, bounded sample of cfg1 shifts."""
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    try:
-        from threadpoolctl import threadpool_limits
-        lim = threadpool_limits(1)
-    except Exception:  # noqa: BLE001
-        lim = None
-    from oracle import engine_ref
-
-    H = build_cfg1()
-    (lo, hi), _ = cfg1_interval()
-    cache = {}
-    engine_ref.inertia(H, 0.0, skel_cache=cache)  # warm the skeleton cache
+    w = Workload()
+    w.name = "cfg1"
     t0 = time.perf_counter()
-    n = 0
-    while time.perf_counter() - t0 < seconds:
-        engine_ref.inertia(H, float(shifts_for(lo, hi, 1, 7, n)[0]), skel_cache=cache)
-        n += 1
-    dt = time.perf_counter() - t0
-    if lim is not None:
-        lim.unregister() if hasattr(lim, "unregister") else None
-    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{n} single-shift factorizations of cfg1 in {dt:.1f} s "
-                      f"(oracle/engine_ref.py, 1 thread)"}
+    cloud, kern, tree, st = configs.config_problem("cfg1", seed=0)
+    w.H = construct(kern, tree, st, configs.CONFIGS["cfg1"].eps)
+    w.host_H = w.H
+    w.construct_s = time.perf_counter() - t0
+    z = np.load(os.path.join(ROOT, "tests", "golden", "cfg1.npz"))
+    w.interval = tuple(float(v) for v in z["interval"])
+    w.eigs = z["eigs"]
+    w.n = cloud.n
+    w.k = w.n // 2
+    w.config = {"workload": "cfg1", "n": w.n, "kernel": "1/r (A_ii = 0)", "leaf": 128,
+                "eta": 1.0, "eps": 1e-8, "eps_ev": EPS_EV, "k": w.k,
+                "interval": "reference Gershgorin interval (tests/golden/cfg1.npz)"}
+    return w
+
+
+def make_workload(name):
+    return workload_cfg2() if name == "cfg2" else workload_cfg1()
+
+
+def rounds_needed(interval, eps_ev, q):
+    levels = math.ceil(math.log2((interval[1] - interval[0]) / eps_ev))
+    return levels, math.ceil(levels / q)
+
+
+# ------------------------------------------------------------ oracle samples
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        return max([d.get("num_threads", 1) for d in threadpool_info()] or [1])
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+def oracle_sample(host_H, mu, seconds, cache):
+    """First `seconds` of one oracle factorization -> (elim_flops done, seconds, clusters, full)."""
+    from oracle import engine_ref
+
+    eng = engine_ref.OracleEngine(host_H, host_H.shift + mu, cache, deadline_s=seconds)
+    t0 = time.perf_counter()
+    try:
+        eng.run()
+        return eng.elim_flops, time.perf_counter() - t0, eng._nclus, True
+    except engine_ref.Deadline as d:
+        return d.elim_flops, d.seconds, d.clusters, False
+    except engine_ref.ShiftHit:
+        return eng.elim_flops, time.perf_counter() - t0, eng._nclus, False
+
+
+def cpu_baseline(wl, mus, elim_per_eval, seconds):
+    """Oracle port on the host, bounded sample, scaled to evaluations/s."""
+    from paper_2311_08618_b200 import gpu_build
+
+    t0 = time.perf_counter()
+    host_H = wl.host_H if wl.host_H is not None else gpu_build.to_host(wl.H)
+    cache = {}
+    # warm the per-origin skeleton cache (shift independent, cached by the reference too)
+    from oracle import engine_ref
+
+    eng = engine_ref.OracleEngine(host_H, host_H.shift + float(mus[0]), cache, deadline_s=0.0)
+    try:
+        eng.run()
+    except (engine_ref.Deadline, engine_ref.ShiftHit):
+        pass
+    setup = time.perf_counter() - t0
+    if wl.name == "cfg1":  # whole factorizations fit the budget
+        t0 = time.perf_counter()
+        n = 0
+        while time.perf_counter() - t0 < seconds:
+            engine_ref.inertia(host_H, float(mus[n % len(mus)]), skel_cache=cache)
+            n += 1
+        dt = time.perf_counter() - t0
+        return {"value": n / dt, "unit": UNIT, "cores": _blas_threads(), "kind": "port",
+                "sample": f"{n} whole single-shift factorizations of cfg1 in {dt:.1f} s "
+                          f"(oracle/engine_ref.py)"}
+    fl, dt, nc, full = oracle_sample(host_H, float(mus[0]), seconds, cache)
+    rate = fl / dt
+    return {"value": rate / elim_per_eval, "unit": UNIT, "cores": _blas_threads(), "kind": "port",
+            "sample": f"first {dt:.1f} s of one cfg2 factorization at mu={float(mus[0]):.6g} "
+                      f"({nc} leaf clusters eliminated, {fl / 1e12:.2f} of "
+                      f"{elim_per_eval / 1e12:.1f} elimination TFLOP; oracle/engine_ref.py on "
+                      f"the same H exported to host memory), scaled by the flop fraction",
+            "elim_gflops_per_s": rate / 1e9, "extrapolated": True,
+            "setup_s": setup}
 
 
 # ----------------------------------------------------------------------- ours
+class _Stop(Exception):
+    pass
+
+
 def run_ours(args):
     import torch
 
@@ -221,128 +275,308 @@ def run_ours(args):
 
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     torch.cuda.set_device(local)
-    from paper_2311_08618_b200 import _native, inertia_batch
+    from paper_2311_08618_b200 import _native, inertia_batch, multisection
+    from paper_2311_08618_b200.bisection import InertiaCache
     from paper_2311_08618_b200.ldl import ldl_counts_array
 
     _native.set_default_device(local)
-    H = build_cfg1()
-    (lo, hi), eigs = cfg1_interval()
+    wl = make_workload(args.config)
+    H = wl.H
+    S = args.batch or (7 if wl.name == "cfg2" else 255)
     eng = _native.engine_for(H, local)
-    eng.set_option("max_batch", args.batch)
+    eng.set_option("max_batch", S)
+    eng.set_option("concurrency", 1)
     eng.set_option("time_kernels", 1)
-    S = args.batch
-    for w in range(max(3, args.warmup)):
-        ldl_counts_array(H, shifts_for(lo, hi, S, w, rank))
-    # ---- device-timed region
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    clocks.start()
-    ms = 0.0
-    ms_schur = 0.0
-    schur_flops = 0.0
-    schur_bytes = 0.0
-    gemm_exec = 0.0
-    flops = 0.0
-    launches = 0
-    ok = True
-    for k in range(args.steps):
-        mus = shifts_for(lo, hi, S, 100 + k, rank)
+    W = max(3, args.warmup)
+    K = args.steps
+    steps = []          # (phase, mus, stats)
+    state = {"phase": "warm", "n": 0}
+
+    def local_eval(mus):
         counts, status, st = ldl_counts_array(H, mus)
-        ms += st["ms_total"]
-        ms_schur += st["ms_schur"]
-        schur_flops += st["schur_flops"]
-        schur_bytes += st["bytes"]
-        gemm_exec += st["gemm_flops_exec"]
-        flops += st["flops"]
-        launches += st["launches"]
-        if k == 0:  # spot-check against the exact spectrum (rank-0 H2: exact matrix)
-            want = np.searchsorted(eigs, mus)
-            ok = ok and bool(np.array_equal(counts[:, 0], want)) and not status.any()
-    torch.cuda.synchronize()
-    clk = clocks.stop()
-    t_dev = ms / 1e3
+        neg = counts[:, 0].copy()
+        bad = [q for q in range(len(mus)) if status[q] or counts[q, 1]]
+        if bad:  # shift on an eigenvalue: the reference's retry (rare)
+            fix = inertia_batch(H, [mus[q] for q in bad])
+            for q, c in zip(bad, fix):
+                neg[q] = c.neg
+        steps.append((state["phase"], list(mus), st))
+        return [int(v) for v in neg]
+
     if world > 1:
-        tt = torch.tensor([t_dev], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_dev = float(tt.item())
-    value = world * S * args.steps / t_dev
-    # ---- e2e through the public API (host shifts in, host counts out)
+        from paper_2311_08618_b200.multigpu import ShardedEvaluator
+
+        sharded = ShardedEvaluator(local_eval=local_eval)
+    else:
+        sharded = local_eval
+    marks = {}
+
+    def evaluate(mus):
+        if state["phase"] == "warm" and state["n"] == W:
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            state["phase"] = "timed"
+            marks["clock"] = ClockSampler(local)
+            marks["clock"].start()
+            marks["t0"] = time.perf_counter()
+        elif state["phase"] == "timed" and state["n"] == W + K:
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            marks["t1"] = time.perf_counter()
+            raise _Stop()
+        state["n"] += 1
+        return sharded(mus)
+
+    cache = InertiaCache()
+    try:
+        multisection(H, [wl.k], wl.interval, EPS_EV, cache=cache, batch=S * world,
+                     evaluate=evaluate)
+    except _Stop:
+        pass
+    if "t1" not in marks:  # search converged before W + K rounds (small configs)
+        torch.cuda.synchronize()
+        marks["t1"] = time.perf_counter()
+    clk = marks["clock"].stop() if "clock" in marks else None
+    timed = [st for ph, _, st in steps if ph == "timed"]
+    timed_mus = [m for ph, m, _ in steps if ph == "timed"]
+    ms = sum(st["ms_total"] for st in timed)
+    ms_schur = sum(st["ms_schur"] for st in timed)
+    schur_flops = sum(st["schur_flops"] for st in timed)
+    elim = sum(st["elim_flops"] for st in timed)
+    flops = sum(st["flops"] for st in timed)
+    gemm_exec = sum(st["gemm_flops_exec"] for st in timed)
+    launches = sum(st["launches"] for st in timed)
+    mem_peak = max([st["mem_peak"] for st in timed] or [0])
+    kinds = np.sum([st["ms_kind"] for st in timed], axis=0).tolist() if timed else None
+    n_local = sum(len(m) for m in timed_mus)
+    t_dev = ms / 1e3
+    n_all = n_local
+    if world > 1:
+        tt = torch.tensor([t_dev, float(n_local)], dtype=torch.float64, device="cuda")
+        mx = tt.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = tt.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        t_dev, n_all = float(mx[0].item()), int(sm[1].item())
+    value = n_all / t_dev if t_dev > 0 else None
+    # ---- one shift per step (the sequential bisection mode), two rounds
+    single = []
+    for mu in (timed_mus[-1][:2] if timed_mus else [0.0, 1.0]):
+        counts, status, st = ldl_counts_array(H, [mu])
+        single.append(st["ms_total"])
+    single_rate = len(single) / (sum(single) / 1e3)
+    # ---- e2e: the timed shift lists again through the public API
     if world > 1:
         dist.barrier()
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for k in range(args.steps):
-        inertia_batch(H, list(shifts_for(lo, hi, S, 200 + k, rank)))
+    for mus in timed_mus:
+        inertia_batch(H, mus)
+    torch.cuda.synchronize()
     t_e2e = time.perf_counter() - t0
     if world > 1:
         tt = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_e2e = float(tt.item())
-    e2e = world * S * args.steps / t_e2e
+    e2e = n_all / t_e2e if t_e2e > 0 else None
+    # ---- eigenvalue: projection from the measured rounds; --eig runs the search
+    q = max(1, int(math.floor(math.log2(S * world + 1))))
+    levels, nrounds = rounds_needed(wl.interval, EPS_EV, q)
+    step_s = t_dev / max(1, len(timed))
+    eig = {"k": wl.k, "eps_ev": EPS_EV, "bisection_levels": levels,
+           "multisection_rounds": nrounds, "shifts_per_round": S * world,
+           "s_per_eigenvalue_multisection": nrounds * step_s,
+           "s_per_eigenvalue_sequential": levels * (sum(single) / 1e3 / max(1, len(single))),
+           "projected": True,
+           "rule": "rounds x measured device seconds per round (multisection, S shifts/round);"
+                   " levels x measured one-shift step (sequential bisection)"}
+    if args.eig:
+        eng.set_option("time_kernels", 0)
+        ks = [1, wl.k, wl.n] if wl.name == "cfg2" else [wl.k]
+        ev = sharded if world > 1 else (lambda mus: local_eval(mus))
+        state["phase"] = "eig"
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        ests = multisection(H, ks, wl.interval, EPS_EV, cache=InertiaCache(),
+                            batch=S * world, evaluate=ev)
+        t_eig = time.perf_counter() - t0
+        eig["measured"] = {"ks": ks, "wall_s": t_eig, "s_per_eigenvalue": t_eig / len(ks),
+                           "values": [e.value for e in ests],
+                           "evals": [e.inertia_evals for e in ests]}
+        if wl.eigs is not None:
+            eig["measured"]["abs_err_vs_eigvalsh"] = [abs(e.value - float(wl.eigs[e.k - 1]))
+                                                       for e in ests]
     if rank != 0:
         dist.destroy_process_group()
         return
     peak = measure_fp64_peak(torch, "cuda")
     achieved = schur_flops / (ms_schur / 1e3) / 1e12 if ms_schur > 0 else None
-    # ---- seconds per eigenvalue (k = n/2, eps_ev = 1e-8), sequential and multisection
-    from paper_2311_08618_b200 import multisection, slice_spectrum
-
-    eng.set_option("time_kernels", 0)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    est = slice_spectrum(H, 1024, (lo, hi), 1e-8)
-    t_seq = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    (mest,) = multisection(H, [1024], (lo, hi), 1e-8, batch=63)
-    t_ms = time.perf_counter() - t0
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": len(timed),
+        "warmup": W, "ms_per_step": 1e3 * t_dev / max(1, len(timed)), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg1", "n": 2048, "leaf": 128, "kernel": "1/r", "eps": 1e-8,
-                   "shifts_per_step": S, "parallelism": f"shift-replicas x{world}",
-                   "l2": "inputs larger than L2 (s x 17.8 MB per step)"},
-        "roofline": {"bound": "tensor", "kernel": "gemm_kernel (Schur update, DMMA fp64)",
+        "config": dict(wl.config, shifts_per_step=S * world, shifts_per_rank=S,
+                       parallelism=f"shift-sharded multisection x{world} (NCCL all-gather of counts)"
+                       if world > 1 else "single GPU",
+                       l2="inputs larger than L2 (H 12.3 GB + ~16 GB per shift of working blocks)"
+                       if wl.name == "cfg2" else "inputs larger than L2"),
+        "roofline": {"bound": "tensor", "kernel": "schur_gemm_kernel (K6 Schur update, DMMA fp64)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": None,
                      "peak_source": "measured in-run: cuBLAS DGEMM fp64 8192^3 best of 5 "
                                     "(MEASURED_PEAKS.json has no fp64 figure)",
                      "schur_share_of_step": ms_schur / ms if ms else None,
-                     "algorithmic_flops_per_eval": schur_flops / (S * args.steps),
-                     "algorithmic_bytes_per_eval": schur_bytes / (S * args.steps),
-                     "flops_rule": "SURVEY.md §8d: Schur 2 nR [sum_{a<b} l_a l_b + 1/2 sum_a l_a^2] "
-                                   "per elimination step, live rows only"},
-        "step_rates": {"algorithmic_tflops": flops / t_dev / 1e12 / max(1, 1),
-                       "dmma_executed_tflops": gemm_exec / (ms / 1e3) / 1e12 if ms else None},
+                     "algorithmic_flops_per_eval": schur_flops / max(1, n_local),
+                     "flops_rule": "SURVEY.md §8d: Schur n_R R^2 per elimination step "
+                                   "(R = live rows of the panel)"},
+        "step_rates": {"algorithmic_tflops": flops / t_dev / 1e12 if t_dev else None,
+                       "elimination_tflops": elim / t_dev / 1e12 if t_dev else None,
+                       "dmma_executed_tflops": gemm_exec / (ms / 1e3) / 1e12 if ms else None,
+                       "ms_by_kind": dict(zip(["panel_gemm", "schur_gemm", "rotation_merge_gemm",
+                                               "bk", "panel_solve", "copies", "recompression_qr",
+                                               "unused"], kinds)) if kinds else None,
+                       "device_mem_peak_gb": mem_peak / 1e9},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * S,
                 "d2h_bytes_per_step": (3 * 8 + 4) * S},
         "gpu_launches": launches,
         "clocks": clk,
-        "parity_spot_check": ok,
-        "eigenvalue": {"k": 1024, "eps_ev": 1e-8, "sequential_s": t_seq,
-                       "sequential_evals": est.inertia_evals, "multisection_s": t_ms,
-                       "multisection_evals": mest.inertia_evals,
-                       "value": est.value, "multisection_equal": mest.value == est.value,
-                       "abs_err_vs_eigvalsh": abs(est.value - float(eigs[1023]))},
-        "algorithmic_flops_per_step": flops / args.steps,
+        "single_shift": {"value": single_rate, "unit": UNIT, "ms_per_step": float(np.mean(single))},
+        "eigenvalue": eig,
+        "construction_s": wl.construct_s,
+        "elim_flops_per_eval": elim / max(1, n_local),
     }
-    if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_sample(args.cpu_seconds)
+    if wl.eigs is not None and timed_mus:
+        want = np.searchsorted(wl.eigs, timed_mus[0])
+        got = [c.neg for c in inertia_batch(H, timed_mus[0])]
+        line["parity_spot_check"] = bool(np.array_equal(np.asarray(got), want))
+    if world == 1 and not args.no_cpu_baseline:
+        mus = timed_mus[0] if timed_mus else [0.0]
+        line["cpu_baseline"] = cpu_baseline(wl, mus, elim / max(1, n_local), args.cpu_seconds)
+    if wl.name == "cfg2":
+        try:
+            with open(WORKLOAD_FILE, "w") as f:
+                json.dump({"elim_flops_per_eval": elim / max(1, n_local),
+                           "interval": list(wl.interval), "first_round": timed_mus[0]
+                           if timed_mus else None}, f)
+        except OSError:
+            pass
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------------------ reference
+def _ref_cfg1_worker(args):
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    mus, = args
+    from paper_2311_08618_b200 import configs, construct
+    from oracle import engine_ref
+
+    cloud, kern, tree, st = configs.config_problem("cfg1", seed=0)
+    H = construct(kern, tree, st, configs.CONFIGS["cfg1"].eps)
+    cache = {}
+    return [engine_ref.inertia(H, float(mu), skel_cache=cache) for mu in mus]
+
+
+def _dyadic_round(interval, q):
+    a, b = interval
+    pts = []
+    for lv in range(1, q + 1):
+        for j in range(1, 2 ** lv, 2):
+            pts.append(a + (b - a) * j / 2 ** lv)
+    return pts
+
+
+def run_reference(args):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return
+    W, K = max(3, args.warmup), args.steps
+    if args.config == "cfg1":
+        import multiprocessing as mp
+
+        for var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ[var] = "1"
+        cores = os.cpu_count() or 1
+        z = np.load(os.path.join(ROOT, "tests", "golden", "cfg1.npz"))
+        lo, hi = (float(v) for v in z["interval"])
+        rng = np.random.default_rng(0)
+        ctx = mp.get_context("spawn")
+        with ctx.Pool(cores) as pool:
+            pool.map(_ref_cfg1_worker, [([0.0],)] * cores)
+            for _ in range(W):
+                pool.map(_ref_cfg1_worker, [([rng.uniform(lo, hi)],) for _ in range(cores)])
+            t0 = time.perf_counter()
+            for _ in range(K):
+                pool.map(_ref_cfg1_worker, [([rng.uniform(lo, hi)],) for _ in range(cores)])
+            dt = time.perf_counter() - t0
+        v = cores * K / dt
+        sample = (f"{cores} worker processes x 1 whole factorization per step "
+                  f"(oracle/engine_ref.py, OPENBLAS_NUM_THREADS=1)")
+        cfg = {"workload": "cfg1", "n": 2048, "leaf": 128, "eps": 1e-8}
+    else:
+        from paper_2311_08618_b200 import gpu_build
+        from oracle import engine_ref
+
+        wl = workload_cfg2()
+        # the input H is built on the device (the CPU construction takes ~500 s); the
+        # timed path -- the factorization -- is the oracle port on the host
+        host_H = gpu_build.to_host(wl.H)
+        del wl.H
+        try:
+            with open(WORKLOAD_FILE) as f:
+                elim_per_eval = float(json.load(f)["elim_flops_per_eval"])
+            src = WORKLOAD_FILE
+        except (OSError, KeyError, ValueError):
+            elim_per_eval = 5.31e13
+            src = "built-in constant (device run of round 1)"
+        mus = _dyadic_round(wl.interval, 3)
+        cache = {}
+        eng = engine_ref.OracleEngine(host_H, mus[0], cache, deadline_s=0.0)
+        try:
+            eng.run()
+        except (engine_ref.Deadline, engine_ref.ShiftHit):
+            pass
+        per = args.ref_seconds
+        for s in range(W):
+            oracle_sample(host_H, mus[s % len(mus)], per, cache)
+        fl_tot, t_tot = 0.0, 0.0
+        for s in range(K):
+            fl, dt, nc, full = oracle_sample(host_H, mus[(W + s) % len(mus)], per, cache)
+            fl_tot += fl
+            t_tot += dt
+        v = fl_tot / t_tot / elim_per_eval
+        cores = _blas_threads()
+        sample = (f"each step = first {per:.0f} s of one cfg2 factorization (oracle/engine_ref.py, "
+                  f"numpy BLAS on {cores} threads, same H exported to host), scaled by the "
+                  f"elimination-flop fraction (total per evaluation from {src})")
+        cfg = dict(wl.config)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": K, "warmup": W, "ms_per_step": 1e3 / v if v else None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": cfg,
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg1", choices=["cfg1"])
-    ap.add_argument("--batch", type=int, default=256)
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg1"])
+    ap.add_argument("--batch", type=int, default=0, help="shifts per GPU per step")
+    ap.add_argument("--eig", action="store_true", help="run the eigenvalue searches to the end")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--ref-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

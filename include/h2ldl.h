@@ -107,6 +107,7 @@ typedef struct h2l_stats {
                              5 copies, 6 recompression QR, 7 unused */
     double ms_host;       /* wall-clock ms of the call on the host */
     double mem_peak;      /* bytes: high-water mark of the waves' device pools during the call */
+    double elim_flops;    /* the elimination part of `flops` (BK + panel + Schur, live rows) */
 } h2l_stats;
 
 int h2l_create(h2l_engine **engine, int device);

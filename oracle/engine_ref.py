@@ -20,6 +20,7 @@ Structure of one run (reference line numbers):
   * retry wrapper with mu <- mu(1+d)+d                              gldl.py:615-633
 """
 
+import time
 from collections import defaultdict
 from itertools import combinations
 
@@ -38,6 +39,14 @@ class ShiftHit(Exception):
 
 class Unstable(Exception):
     pass
+
+
+class Deadline(Exception):
+    """Bounded-sample stop (bench cpu_baseline): work done when the time ran out."""
+
+    def __init__(self, elim_flops, seconds, clusters):
+        super().__init__(f"deadline after {clusters} clusters, {seconds:.1f} s")
+        self.elim_flops, self.seconds, self.clusters = elim_flops, seconds, clusters
 
 
 def abs_split(G, tol):
@@ -64,7 +73,10 @@ def _key(a, b):
 class OracleEngine:
     """One factorization of origin(H) - shift*I; counts accumulate in self.counts."""
 
-    def __init__(self, H, shift, skel_cache=None):
+    def __init__(self, H, shift, skel_cache=None, deadline_s=None):
+        self.deadline_s = deadline_s
+        self.elim_flops = 0.0   # survey §8d count, live rows (== the engine's elim_flops)
+        self.done = set()       # eliminated clusters of the current level
         self.H = H.origin()
         self.tree = self.H.tree
         self.st = self.H.structure
@@ -102,6 +114,8 @@ class OracleEngine:
             self._root(self._skel_diag(0))
             return self
         self._leaf_level()
+        self._t0 = time.perf_counter()
+        self._nclus = 0
         level = self.tree.depth
         while True:
             self._sweep(level)
@@ -142,10 +156,16 @@ class OracleEngine:
 
     # ------------------------------------------------------------ level sweep
     def _sweep(self, level):
+        self.done = set()
         for i in range(self.tree.num_clusters(level)):
             if self.node[i].m:
                 self._recompress(i)
                 self._eliminate(i)
+                self._nclus += 1
+                if self.deadline_s is not None:
+                    dt = time.perf_counter() - self._t0
+                    if dt > self.deadline_s:
+                        raise Deadline(self.elim_flops, dt, self._nclus)
         low = set(self.st.lowrank_at(level))
         for key in [k for k in self.fl if k in low]:
             a, b = key
@@ -216,6 +236,10 @@ class OracleEngine:
             X = np.linalg.solve(f.D, W.T).T
         else:
             W = X = np.zeros((0, nR))
+        # algorithmic count on live rows: BK nR^3/3, panel R nR^2 + R nR, Schur nR R^2
+        live = nd.nS + sum(self.node[j].m - (self.node[j].nR if j in self.done else 0)
+                           for j in partners)
+        self.elim_flops += nR ** 3 / 3.0 + live * nR * nR + live * nR + nR * float(live) ** 2
         seg = {i: (0, nd.nS)}
         pos = nd.nS
         for j in partners:
@@ -253,6 +277,7 @@ class OracleEngine:
                 self.off[k][:nR, :] = 0.0
             else:
                 self.off[k][:, :nR] = 0.0
+        self.done.add(i)
 
     # ------------------------------------------------------------------ merge
     def _content(self, key):

@@ -54,6 +54,7 @@ class Stats(ctypes.Structure):
         ("launches", ctypes.c_int64), ("schur_flops", ctypes.c_double),
         ("gemm_flops_exec", ctypes.c_double), ("ms_kind", ctypes.c_double * 8),
         ("ms_host", ctypes.c_double), ("mem_peak", ctypes.c_double),
+        ("elim_flops", ctypes.c_double),
     ]
 
     def as_dict(self):

@@ -1185,6 +1185,7 @@ private:
             release(Xb);
         }
         st_acc_->flops += flops * s_;
+        st_acc_->elim_flops += flops * s_;
         // ---- retire the redundant rows / columns of i (gldl.py:411-417).  The
         // reference zeroes them; here every block of i is compacted to its skeleton
         // rows / columns (the R part is zero from now on and never read again), and i
@@ -1497,6 +1498,7 @@ static void merge_stats(h2l_stats &a, const h2l_stats &b) {
     a.max_front = std::max(a.max_front, b.max_front);
     a.dropped_fro += b.dropped_fro;
     a.flops += b.flops;
+    a.elim_flops += b.elim_flops;
     a.bytes += b.bytes;
     a.ms_schur += b.ms_schur;
     a.ms_bk += b.ms_bk;

@@ -321,20 +321,60 @@ class DeviceBasis(BasisSplit):
 
 
 def to_host(H):
-    """Copy a device-built H into an ordinary numpy RankStructuredMatrix."""
-    def h(v):
+    """Copy a device-built H into an ordinary numpy RankStructuredMatrix.
+
+    The arena crosses PCIe once; blocks become numpy views of the host copy."""
+    arena = getattr(H, "_arena", None)
+    offs = getattr(H, "_arena_offsets", None)
+    if arena is not None and offs is not None:
+        host = arena.detach().cpu().numpy()
+
+        def hv(kind, key, shape):
+            o = offs[(kind, key)]
+            return host[o:o + shape[0] * shape[1]].reshape(shape)
+    else:
+        hv = None
+
+    def h(kind, key, v):
+        if hv is not None and (kind, key) in offs:
+            return hv(kind, key, tuple(v.shape))
         return v.detach().cpu().numpy().copy()
 
     bases = {}
     for k, b in H.bases.items():
-        sq = h(b.square())
+        sq = h("B", k, b.square())
         m, r = sq.shape[0], b.rank
         bases[k] = BasisSplit(U_S=sq[:, m - r:].copy(), U_R=sq[:, :m - r].copy())
-    return RankStructuredMatrix(
+    out = RankStructuredMatrix(
         fmt=H.fmt, tree=H.tree, structure=H.structure, eps=H.eps,
-        leaf_diag={k: h(v) for k, v in H.leaf_diag.items()},
-        leaf_offdiag={k: h(v) for k, v in H.leaf_offdiag.items()},
-        bases=bases, couplings={k: h(v) for k, v in H.couplings.items()})
+        leaf_diag={k: h("D", k, v) for k, v in H.leaf_diag.items()},
+        leaf_offdiag={k: h("O", k, v) for k, v in H.leaf_offdiag.items()},
+        bases=bases, couplings={k: h("C", k, v) for k, v in H.couplings.items()})
+    return out
+
+
+def gershgorin_device(kernel, rows=1024, pad=1e-6, device="cuda"):
+    """Search interval of BASELINE's configs: Gershgorin discs of the kernel matrix.
+
+    Row sums of |A_ij| are evaluated on the device in row slabs (the n x n
+    matrix is never stored).  The H2 approximation differs from A by about
+    eps * |A|, so both ends are widened by pad * max(|lo|, |hi|)."""
+    t = _torch()
+    K = DeviceKernel(kernel, device)
+    n = kernel.cloud.n if kernel.kind is not None else K.A.shape[0]
+    lo, hi = np.inf, -np.inf
+    for i0 in range(0, n, rows):
+        i1 = min(n, i0 + rows)
+        rad = t.zeros(i1 - i0, dtype=t.float64, device=K.dev)
+        for j0 in range(0, n, SLAB):
+            j1 = min(n, j0 + SLAB)
+            rad += K.block(i0, i1, j0, j1).abs().sum(dim=1)
+        d = t.diagonal(K.block(i0, i1, i0, i1))
+        rad -= d.abs()
+        lo = min(lo, float((d - rad).min()))
+        hi = max(hi, float((d + rad).max()))
+    w = pad * max(abs(lo), abs(hi), 1.0)
+    return lo - w, hi + w
 
 
 def config_device(name, seed=0, n=None, leaf=None, device="cuda", verbose=False):
@@ -343,4 +383,6 @@ def config_device(name, seed=0, n=None, leaf=None, device="cuda", verbose=False)
 
     cfg = configs.CONFIGS[name]
     cloud, kern, tree, st = configs.config_problem(name, seed=seed, n=n, leaf=leaf)
-    return construct_device(kern, tree, st, cfg.eps, device=device, verbose=verbose), cloud
+    H = construct_device(kern, tree, st, cfg.eps, device=device, verbose=verbose)
+    H._kernel = kern
+    return H, cloud

@@ -79,3 +79,19 @@ def test_mini_config3_device_build():
     mus = [float(0.5 * (w[k] + w[k + 1])) for k in (10, 700, 1023, 1500, 2040)]
     got = [c.neg for c in inertia_batch(Hd, mus)]
     assert got == [11, 701, 1024, 1501, 2041]
+
+
+def test_gershgorin_device_and_arena_export():
+    Hd, cloud = gpu_build.config_device("cfg1", n=1024, leaf=64)
+    kern = Hd._kernel
+    A = kern.block(np.arange(cloud.n), np.arange(cloud.n))
+    lo, hi = h2matrix.gershgorin_interval(A)
+    glo, ghi = gpu_build.gershgorin_device(kern, rows=300, pad=0.0)
+    assert glo == pytest.approx(lo, rel=1e-12) and ghi == pytest.approx(hi, rel=1e-12)
+    plo, phi = gpu_build.gershgorin_device(kern)
+    assert plo < lo and phi > hi
+    Hh = gpu_build.to_host(Hd)
+    for k, v in Hd.leaf_offdiag.items():
+        assert np.array_equal(Hh.leaf_offdiag[k], v.cpu().numpy())
+    for k, b in Hd.bases.items():
+        assert np.array_equal(Hh.bases[k].square(), b.square().cpu().numpy())

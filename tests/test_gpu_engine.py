@@ -191,3 +191,17 @@ def test_cfg1_multisection_over_nccl_world1(cfg1):
     assert ests[0].value == float(z["estimate"][0])
     assert abs(ests[1].value - z["eigs"][0]) <= 1e-8
     assert ev.rounds > 0 and ev.world == 1
+
+
+@pytest.mark.parametrize("name", instance_names()[:6])
+def test_engine_elimination_flops_match_oracle(name):
+    """The survey §8d flop count the bench's roofline and CPU-sample scaling use is
+    the same number on the device engine and in the oracle (same H, same shift)."""
+    from oracle import engine_ref
+    from paper_2311_08618_b200.ldl import ldl_counts_array
+
+    H = h2matrix.load_payload(f"tests/golden/h_{name}.npz")
+    mu = float(golden(f"counts_{name}.npz")["mus"][0])
+    _, _, st = ldl_counts_array(H, [mu])
+    want = engine_ref.OracleEngine(H, mu, {}).run().elim_flops
+    assert st["elim_flops"] == pytest.approx(want, rel=1e-12)

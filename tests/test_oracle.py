@@ -130,3 +130,18 @@ def test_cfg1_oracle_replays_reference_trace():
     for row in trace[[0, 7, 19, 39]]:
         mu = float(row[0])
         assert engine_ref.inertia(H, mu, skel_cache=cache) == tuple(int(v) for v in row[1:])
+
+
+def test_oracle_deadline_sample_counts_elimination_flops():
+    """bench.py's bounded CPU sample: a deadline stops the run after whole clusters
+    and reports the elimination flops done so far (a prefix of the full count)."""
+    name = SMALL[0]
+    H = h2matrix.load_payload(f"tests/golden/h_{name}.npz")
+    mu = float(golden(f"counts_{name}.npz")["mus"][0])
+    cache = {}
+    full = engine_ref.OracleEngine(H, mu, cache).run()
+    assert full.elim_flops > 0
+    with pytest.raises(engine_ref.Deadline) as ex:
+        engine_ref.OracleEngine(H, mu, cache, deadline_s=0.0).run()
+    d = ex.value
+    assert d.clusters == 1 and 0 < d.elim_flops <= full.elim_flops
