@@ -125,7 +125,12 @@ int h2l_upload(h2l_engine *engine, const h2l_plan *plan);
 int h2l_inertia(h2l_engine *engine, const double *mu, int32_t s, int64_t *counts,
                 int32_t *status, h2l_stats *stats);
 
-/* Tuning knobs (key, value): "max_batch" shifts per device wave (default 64). */
+/*
+ * Tuning knobs (key, value): "max_batch" shifts per device wave (default 64);
+ * "concurrency" waves in flight on private streams (default 2); "time_kernels"
+ * 0 off, 1 CUDA-event timing of every launch kind (stats.ms_kind), 2 the Schur
+ * GEMM launches only (stats.ms_schur; negligible overhead).
+ */
 int h2l_set_option(h2l_engine *engine, const char *key, int64_t value);
 
 /*

@@ -100,7 +100,8 @@ void launch_copy_prefixed(const CopyTask *dev_tasks, const int *dev_prefix, int 
 
 int gemm_tiles(int M, int N);
 void launch_gemm(const GemmTask *dev_tasks, const int *dev_tile_prefix, int ntasks,
-                 int total_tiles, int nshift, cudaStream_t st, bool schur = false);
+                 int total_tiles, int nshift, cudaStream_t st, bool schur = false,
+                 const int *dev_tile_task = nullptr);
 
 int64_t bk_scratch_doubles(int n);
 cudaError_t launch_bk_engine(const BkJob *dev_jobs, int njobs, int nshift, int nmax,
@@ -129,6 +130,13 @@ cudaError_t launch_tail_rank(const double *DT, int64_t dstride, int c, int n, do
                              const double *tol, int *rank, double *dropped, int *r1out,
                              const int *active, int nshift, cudaStream_t st);
 int64_t tail_rank_part_doubles(int c, int n);
+// cluster-parallel full pivoted QR of an n x n Gram matrix (reflectors to rows of M)
+int pqr_cluster_size(int n);
+cudaError_t launch_pqr_cluster(double *M, int64_t mstride, int n, double *tau, int *piv,
+                               int64_t vstride, const int *active, int nshift, cudaStream_t st);
+cudaError_t launch_form_q_rows(const double *V, int64_t vstride, int n, const double *tau,
+                               int64_t tstride, double *QT, int64_t qstride, const int *active,
+                               int nshift, cudaStream_t st);
 cudaError_t launch_form_tr(const double *GT, int64_t gstride, int ldg, const double *tau,
                            const int *piv, int64_t vstride, int nR, int t, double *Tr,
                            int64_t tstride, const int *active, int nshift, cudaStream_t st);

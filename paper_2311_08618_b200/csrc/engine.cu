@@ -134,7 +134,7 @@ public:
     }
     void set_option(const std::string &k, int64_t v) {
         if (k == "max_batch") max_batch_ = (int)std::max<int64_t>(1, v);
-        else if (k == "time_kernels") time_kernels_ = v != 0;
+        else if (k == "time_kernels") time_kernels_ = (int)v;  // 0 off, 1 every kind, 2 Schur only
         else throw CudaFail(H2L_EINVAL, "unknown option " + k);
     }
 
@@ -260,7 +260,7 @@ private:
     cudaStream_t st_ = nullptr;
     Staging stage_;
     int max_batch_ = 64;
-    bool time_kernels_ = false;
+    int time_kernels_ = 0;
     bool uploaded_ = false;
     cudaEvent_t ev_call_[2];
     std::vector<cudaEvent_t> ev_pool_;
@@ -286,6 +286,7 @@ private:
     int *d_status_ = nullptr, *d_rank_ = nullptr;
     std::vector<Cl> cl_;
     std::vector<Blk> diag_;
+    std::vector<int> tile_map_;
     std::vector<char> elim_, pend_diag_;
     std::set<Pair> pend_off_;
     std::map<Pair, Blk> offd_, coup_, fill_;
@@ -319,8 +320,7 @@ private:
     const void *stage(const void *src, size_t nbytes) {
         const size_t bytes = (nbytes + 255) / 256 * 256;
         if (stage_.off + bytes > stage_.cap) {
-            CK(cudaStreamSynchronize(st_));
-            stage_.off = 0;
+            sync();
             if (bytes > stage_.cap) {
                 stage_.release();
                 stage_.init(bytes * 2);
@@ -382,8 +382,16 @@ private:
         }
     }
     void sync() {
+        const auto t0 = std::chrono::steady_clock::now();
         CK(cudaStreamSynchronize(st_));
+        wait_ms_ += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         stage_.off = 0;
+    }
+    // H2L_HOSTPROF: host time blocked in stream syncs vs the wave's wall time
+    double wait_ms_ = 0.0;
+    static bool hostprof_on() {
+        static const bool on = getenv("H2L_HOSTPROF") != nullptr;
+        return on;
     }
 
     // debug (H2L_DEBUG_GUARD): every block gets GUARD doubles of 0xff canary on both
@@ -522,9 +530,18 @@ private:
         if (!b.t.empty()) {
             const GemmTask *dt = (const GemmTask *)stage(b.t.data(), sizeof(GemmTask) * b.t.size());
             const int *dp = (const int *)stage(b.pre.data(), sizeof(int) * b.pre.size());
+            const int *dm = nullptr;
+            if (b.t.size() > 32) {  // tile -> task map: one load per CTA instead of a search
+                tile_map_.resize(b.tiles);
+                for (size_t q = 0; q < b.t.size(); ++q) {
+                    const int e = q + 1 < b.t.size() ? b.pre[q + 1] : b.tiles;
+                    std::fill(tile_map_.begin() + b.pre[q], tile_map_.begin() + e, (int)q);
+                }
+                dm = (const int *)stage(tile_map_.data(), sizeof(int) * tile_map_.size());
+            }
             {
                 Timed tm(this, kind);
-                launch_gemm(dt, dp, (int)b.t.size(), b.tiles, nshift, st_, kind == 1);
+                launch_gemm(dt, dp, (int)b.t.size(), b.tiles, nshift, st_, kind == 1, dm);
                 if (kind == 1) gemm_hist(b);
             }
             CK(cudaGetLastError());
@@ -546,7 +563,8 @@ private:
     struct Timed {
         Wave *w;
         bool on;
-        Timed(Wave *w_, int kind) : w(w_), on(w_->time_kernels_) {
+        Timed(Wave *w_, int kind)
+            : w(w_), on(w_->time_kernels_ == 1 || (w_->time_kernels_ == 2 && kind == 1)) {
             if (on) CK(cudaEventRecord(w->mark(kind), w->st_));
         }
         ~Timed() {
@@ -587,6 +605,8 @@ private:
 
     // ------------------------------------------------------------------ wave
     void run_wave(const double *mu, int s, int64_t *counts, int32_t *status, h2l_stats &acc) {
+        const auto wall0 = std::chrono::steady_clock::now();
+        wait_ms_ = 0.0;
         s_ = s;
         st_acc_ = &acc;
         ev_used_ = 0;
@@ -662,6 +682,10 @@ private:
         CK(cudaFreeAsync(d_status_, st_));
         CK(cudaFreeAsync(d_rank_, st_));
         sync();
+        if (hostprof_on())
+            fprintf(stderr, "hostprof: wave of %d shifts: wall %.1f ms, blocked in syncs %.1f ms\n", s,
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count(),
+                    wait_ms_);
         st_acc_ = nullptr;
     }
 
@@ -830,6 +854,23 @@ private:
         add_copy(c, cp(src.at(0, nR), src.bs, m, dst.at(0, newR), dst.bs, m, rows, nS));
     }
 
+    // Q^T of the full column-pivoted QR of the n x n Gram matrix M (M is consumed):
+    // the cluster kernel keeps M in distributed shared memory; beyond its capacity
+    // the single-CTA kernel pair runs on M in global memory
+    void gram_order(Blk &M, int n, Blk &QT, double *tau, int *piv, int *used, double *norms,
+                    int64_t ts, const int *d_active) {
+        if (pqr_cluster_size(n)) {
+            CK(launch_pqr_cluster(M.p, M.bs, n, tau, piv, ts, d_active, s_, st_));
+            CK(launch_form_q_rows(M.p, M.bs, n, tau, ts, QT.p, QT.bs, d_active, s_, st_));
+        } else {
+            // M is symmetric: its row-major storage is also its "columns as rows" layout
+            CK(launch_pqr(M.p, M.bs, n, n, n, tau, piv, used, norms, ts, ts, d_tol_, d_rank_,
+                          d_dropped_, d_active, -2, s_, st_));
+            // all n reflectors; with t = n form_tr's row map is the identity (QT = Q^T)
+            CK(launch_form_tr(M.p, M.bs, n, tau, piv, ts, n, n, QT.p, QT.bs, d_active, s_, st_));
+        }
+    }
+
     void recompress(int i) {
         Cl &ci = cl_[i];
         const int nR = ci.nR;
@@ -878,12 +919,7 @@ private:
             }
             {
                 Timed tm(this, 6);
-                // M is symmetric: its row-major storage is also its "columns as rows" layout
-                CK(launch_pqr(M.p, M.bs, nR, nR, nR, tau, piv, used, norms, ts, ts, d_tol_, d_rank_,
-                              d_dropped_, d_active, -2, s_, st_));
-                // all nR reflectors; with t = nR form_tr's row map is the identity (QT = Q^T)
-                CK(launch_form_tr(M.p, M.bs, nR, tau, piv, ts, nR, nR, QT.p, QT.bs, d_active, s_,
-                                  st_));
+                gram_order(M, nR, QT, tau, piv, used, norms, ts, d_active);
             }
             {
                 GemmBatch g;  // D^T = GT Q  (Q[k][n] = QT[n][k])
@@ -920,10 +956,7 @@ private:
                     }
                     {
                         Timed tm(this, 6);
-                        CK(launch_pqr(M2.p, M2.bs, nT, nT, nT, tau, piv, used, norms, ts, ts, d_tol_,
-                                      d_rank_, d_dropped_, d_active, -2, s_, st_));
-                        CK(launch_form_tr(M2.p, M2.bs, nT, tau, piv, ts, nT, nT, Q2T.p, Q2T.bs,
-                                          d_active, s_, st_));
+                        gram_order(M2, nT, Q2T, tau, piv, used, norms, ts, d_active);
                     }
                     {
                         GemmBatch g;  // DT2 = D_tail^T Q2 ; QT2 = Q2^T QT[r1:, :]

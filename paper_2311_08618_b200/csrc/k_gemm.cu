@@ -115,7 +115,8 @@ struct Loader {
 };
 
 template <class Cfg>
-__device__ __forceinline__ void gemm_body(const GemmTask *tasks, const int *prefix, int ntasks) {
+__device__ __forceinline__ void gemm_body(const GemmTask *tasks, const int *prefix, int ntasks,
+                                          const int *tile_task) {
     constexpr int BM = Cfg::BM, BN = Cfg::BN, STAGES = Cfg::STAGES, FM = Cfg::FM, FN = Cfg::FN;
     constexpr int BK = Cfg::BK, SK = Cfg::SK;
     constexpr int THREADS = Cfg::THREADS, CS = Cfg::CS;
@@ -124,7 +125,9 @@ __device__ __forceinline__ void gemm_body(const GemmTask *tasks, const int *pref
     double (*Bs)[BN][SK] = reinterpret_cast<double (*)[BN][SK]>(gsm + STAGES * BM * SK);
     double *Cs = gsm + STAGES * (BM + BN) * SK;
 
-    const int t = find_task(prefix, ntasks, blockIdx.x);
+    // tile -> task: one load from the staged map (large launches) or a binary
+    // search of the tile prefix (small ones)
+    const int t = tile_task ? tile_task[blockIdx.x] : find_task(prefix, ntasks, blockIdx.x);
     const GemmTask tk = tasks[t];
     const int local = blockIdx.x - prefix[t];
     const int tiles_n = (tk.N + BN - 1) / BN;
@@ -244,14 +247,16 @@ __device__ __forceinline__ void gemm_body(const GemmTask *tasks, const int *pref
 
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_kernel(const GemmTask *tasks,
-                                                            const int *prefix, int ntasks) {
-    gemm_body<Cfg>(tasks, prefix, ntasks);
+                                                            const int *prefix, int ntasks,
+                                                            const int *tile_task) {
+    gemm_body<Cfg>(tasks, prefix, ntasks, tile_task);
 }
 // same code under its own name so profiles separate the Schur updates (K6)
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) schur_gemm_kernel(const GemmTask *tasks,
-                                                                  const int *prefix, int ntasks) {
-    gemm_body<Cfg>(tasks, prefix, ntasks);
+                                                                  const int *prefix, int ntasks,
+                                                            const int *tile_task) {
+    gemm_body<Cfg>(tasks, prefix, ntasks, tile_task);
 }
 
 // production configuration (chosen with tools/gemm_bench.py)
@@ -262,7 +267,8 @@ void launch_cfg(const GemmTask *dev_tasks, const int *dev_tile_prefix, int ntask
                 int total_tiles, int nshift, cudaStream_t st) {
     smem_optin(gemm_kernel<Cfg>);
     dim3 grid(total_tiles, nshift);
-    gemm_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(dev_tasks, dev_tile_prefix, ntasks);
+    gemm_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(dev_tasks, dev_tile_prefix, ntasks,
+                                                             nullptr);
 }
 
 }  // namespace
@@ -273,16 +279,19 @@ int gemm_tiles(int M, int N) {
 }
 
 void launch_gemm(const GemmTask *dev_tasks, const int *dev_tile_prefix, int ntasks,
-                 int total_tiles, int nshift, cudaStream_t st, bool schur) {
+                 int total_tiles, int nshift, cudaStream_t st, bool schur,
+                 const int *dev_tile_task) {
     if (ntasks <= 0 || total_tiles <= 0 || nshift <= 0) return;
+    dim3 grid(total_tiles, nshift);
     if (schur) {
         smem_optin(schur_gemm_kernel<Prod>);
-        dim3 grid(total_tiles, nshift);
-        schur_gemm_kernel<Prod><<<grid, Prod::THREADS, Prod::SMEM, st>>>(dev_tasks, dev_tile_prefix,
-                                                                          ntasks);
+        schur_gemm_kernel<Prod><<<grid, Prod::THREADS, Prod::SMEM, st>>>(
+            dev_tasks, dev_tile_prefix, ntasks, dev_tile_task);
         return;
     }
-    launch_cfg<Prod>(dev_tasks, dev_tile_prefix, ntasks, total_tiles, nshift, st);
+    smem_optin(gemm_kernel<Prod>);
+    gemm_kernel<Prod><<<grid, Prod::THREADS, Prod::SMEM, st>>>(dev_tasks, dev_tile_prefix, ntasks,
+                                                               dev_tile_task);
 }
 
 // ---- variants for tools/gemm_bench.py (the tile prefix must use the variant's tiling)

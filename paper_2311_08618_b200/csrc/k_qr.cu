@@ -19,6 +19,8 @@
 // Tr = [U_r^T ; U_s^T] (rows(G) x rows(G)) from the reflectors.
 #include "common.cuh"
 
+#include <cooperative_groups.h>
+
 namespace h2l {
 
 namespace {
@@ -230,6 +232,279 @@ __global__ void __launch_bounds__(QR_THREADS) form_tr_kernel(const double *GT, i
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Cluster-parallel full column-pivoted QR of the n x n Gram matrix M (the
+// recompression's ordering step, engine.cu recompress).  One thread-block
+// cluster of CS CTAs per shift; CTA c keeps columns q = c, c+CS, ... of M in
+// its shared memory (the whole matrix lives in the cluster's distributed
+// shared memory), so a step costs two cluster barriers instead of passes over
+// L2: (1) every CTA publishes the arg-max of its unused column norms and all
+// CTAs reduce the CS candidates (lowest index on ties); (2) the owner of the
+// pivot builds the Householder vector, the others copy it through DSMEM, and
+// every CTA applies it to its own columns and recomputes their trailing norms
+// exactly.  Reflector j is written to row j of M (global; M is dead once
+// staged) as v = [1, x[j+1:]] with tau[j], piv[j] -- the input of form_q_rows.
+namespace cg = cooperative_groups;
+
+constexpr int PQRC_THREADS = 256;
+
+template <int CS>
+__global__ void __launch_bounds__(PQRC_THREADS) pqr_cluster_kernel(double *Mg, int64_t mstride, int n,
+                                                                   double *tau, int *piv,
+                                                                   int64_t vstride,
+                                                                   const int *active) {
+    cg::cluster_group cluster = cg::this_cluster();
+    const int crank = (int)cluster.block_rank();
+    const int z = blockIdx.y;
+    if (active && !active[z]) return;  // uniform over the cluster: no barrier is reached
+    extern __shared__ __align__(16) double qsm[];
+    const int nloc = (n + CS - 1) / CS;
+    double *col = qsm;                          // [nloc][n]
+    double *vbuf = col + (size_t)nloc * n;      // [n]
+    double *nrm = vbuf + n;                     // [nloc]
+    double *slot_v = nrm + nloc;                // [1] candidate value
+    double *red = slot_v + 2;                   // [40]
+    double *hh = red + 40;                      // [4]: tau, scale, beta
+    int *slot_i = (int *)(hh + 4);              // [1] candidate index
+    int *usedl = slot_i + 2;                    // [nloc]
+    int *sp = usedl + nloc;                     // [1] pivot
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+    double *M = Mg + z * mstride;
+    double *tz = tau + z * vstride;
+    int *pz = piv + z * vstride;
+    // stage own columns (M symmetric: column q == row q, contiguous) and norms
+    for (int lc = warp; lc < nloc; lc += nwarp) {
+        const int q = lc * CS + crank;
+        double s2 = 0.0;
+        if (q < n) {
+            for (int r = lane; r < n; r += 32) {
+                const double v = M[(int64_t)q * n + r];
+                col[(size_t)lc * n + r] = v;
+                s2 += v * v;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) s2 += __shfl_down_sync(0xffffffffu, s2, off);
+        if (lane == 0) { nrm[lc] = s2; usedl[lc] = q < n ? 0 : 1; }
+    }
+    cluster.sync();  // every CTA has read M before any reflector overwrites it
+    for (int j = 0; j < n; ++j) {
+        // ---- (1) local arg-max, published in the slot
+        double bv = -1.0;
+        int bi = 0x7fffffff;
+        for (int lc = tid; lc < nloc; lc += blockDim.x) {
+            if (usedl[lc]) continue;
+            const double v = nrm[lc];
+            const int q = lc * CS + crank;
+            if (v > bv || (v == bv && q < bi)) { bv = v; bi = q; }
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+            const double ov = __shfl_down_sync(0xffffffffu, bv, off);
+            const int oi = __shfl_down_sync(0xffffffffu, bi, off);
+            if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+        }
+        if (lane == 0) { red[warp] = bv; ((int *)(red + 20))[warp] = bi; }
+        __syncthreads();
+        if (tid == 0) {
+            double xv = red[0];
+            int xi = ((int *)(red + 20))[0];
+            for (int w = 1; w < nwarp; ++w) {
+                const double ov = red[w];
+                const int oi = ((int *)(red + 20))[w];
+                if (ov > xv || (ov == xv && oi < xi)) { xv = ov; xi = oi; }
+            }
+            *slot_v = xv;
+            *slot_i = xi;
+        }
+        cluster.sync();
+        if (tid == 0) {
+            double xv = -1.0;
+            int xi = 0x7fffffff;
+            for (int c = 0; c < CS; ++c) {
+                const double ov = *cluster.map_shared_rank(slot_v, c);
+                const int oi = *cluster.map_shared_rank(slot_i, c);
+                if (ov > xv || (ov == xv && oi < xi)) { xv = ov; xi = oi; }
+            }
+            *sp = xi;
+        }
+        __syncthreads();
+        const int p = *sp;
+        const int owner = p % CS;
+        // ---- (2) Householder vector at the owner
+        if (owner == crank) {
+            double *x = col + (size_t)(p / CS) * n;
+            double part = 0.0;
+            for (int r = j + 1 + tid; r < n; r += blockDim.x) part += x[r] * x[r];
+#pragma unroll
+            for (int off = 16; off; off >>= 1) part += __shfl_down_sync(0xffffffffu, part, off);
+            if (lane == 0) red[warp] = part;
+            __syncthreads();
+            if (tid == 0) {
+                double xn2 = 0.0;
+                for (int w = 0; w < nwarp; ++w) xn2 += red[w];
+                const double alpha = x[j];
+                double t_, sc, be;
+                if (xn2 == 0.0) { t_ = 0.0; be = alpha; sc = 0.0; }
+                else {
+                    be = -copysign(sqrt(alpha * alpha + xn2), alpha);
+                    t_ = (be - alpha) / be;
+                    sc = 1.0 / (alpha - be);
+                }
+                hh[0] = t_; hh[1] = sc; hh[2] = be;
+                tz[j] = t_;
+                pz[j] = p;
+                usedl[p / CS] = 1;
+            }
+            __syncthreads();
+            const double sc = hh[1];
+            double *vrow = M + (int64_t)j * n;
+            for (int r = j + 1 + tid; r < n; r += blockDim.x) {
+                const double v = x[r] * sc;
+                x[r] = v;
+                vbuf[r] = v;
+                vrow[r] = v;
+            }
+            if (tid == 0) { vbuf[j] = 1.0; x[j] = hh[2]; vrow[j] = 1.0; }
+        }
+        cluster.sync();
+        if (owner != crank) {
+            const double *ov = cluster.map_shared_rank(vbuf, owner);
+            for (int r = j + tid; r < n; r += blockDim.x) vbuf[r] = ov[r];
+            if (tid == 0) hh[0] = *cluster.map_shared_rank(hh, owner);
+        }
+        __syncthreads();
+        // ---- apply H_j = I - tau v v^T to the own unused columns; exact trailing norms
+        const double tj = hh[0];
+        for (int lc = warp; lc < nloc; lc += nwarp) {
+            if (usedl[lc]) continue;
+            double *y = col + (size_t)lc * n;
+            double sdot = 0.0;
+            for (int r = j + lane; r < n; r += 32) sdot += vbuf[r] * y[r];
+#pragma unroll
+            for (int off = 16; off; off >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, off);
+            const double f = tj * sdot;
+            double nn = 0.0;
+            for (int r = j + lane; r < n; r += 32) {
+                const double v = y[r] - f * vbuf[r];
+                y[r] = v;
+                if (r > j) nn += v * v;
+            }
+#pragma unroll
+            for (int off = 16; off; off >>= 1) nn += __shfl_down_sync(0xffffffffu, nn, off);
+            if (lane == 0) nrm[lc] = nn;
+        }
+        __syncthreads();
+    }
+    cluster.sync();  // no CTA exits while its shared memory may still be read
+}
+
+// Q^T of the reflectors in rows of V (row j: v_j = [1 at j, V[j][r] for r > j]):
+// row q of Q^T = (H_0 ... H_{n-1} e_q)^T, built by one warp from e_q with
+// H_j for j = min(q, n-1) .. 0 (H_j e_q = e_q for j > q).  Rows are independent,
+// so the grid spreads them over many CTAs and no barrier is needed.
+constexpr int FQ_WARPS = 8;
+
+__global__ void __launch_bounds__(FQ_WARPS * 32) form_q_rows_kernel(const double *V, int64_t vstr,
+                                                                   int n, const double *tau,
+                                                                   int64_t tstr, double *QT,
+                                                                   int64_t qstr,
+                                                                   const int *active) {
+    extern __shared__ __align__(16) double ybuf[];
+    const int z = blockIdx.y;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int q = blockIdx.x * FQ_WARPS + warp;
+    if (q >= n) return;
+    double *out = QT + z * qstr + (int64_t)q * n;
+    if (active && !active[z]) {
+        for (int r = lane; r < n; r += 32) out[r] = (r == q) ? 1.0 : 0.0;
+        return;
+    }
+    double *y = ybuf + (size_t)warp * n;
+    for (int r = lane; r < n; r += 32) y[r] = (r == q) ? 1.0 : 0.0;
+    __syncwarp();
+    const double *Vz = V + z * vstr;
+    const double *tzz = tau + z * tstr;
+    for (int j = min(q, n - 1); j >= 0; --j) {
+        const double *v = Vz + (int64_t)j * n;
+        double sdot = (lane == 0) ? y[j] : 0.0;
+        for (int r = j + 1 + lane; r < n; r += 32) sdot += v[r] * y[r];
+#pragma unroll
+        for (int off = 16; off; off >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, off);
+        const double f = tzz[j] * sdot;
+        if (lane == 0) y[j] -= f;
+        for (int r = j + 1 + lane; r < n; r += 32) y[r] -= f * v[r];
+        __syncwarp();
+    }
+    for (int r = lane; r < n; r += 32) out[r] = y[r];
+}
+
+size_t pqr_cluster_smem(int n, int cs) {
+    const int nloc = (n + cs - 1) / cs;
+    return sizeof(double) * ((size_t)nloc * n + n + nloc + 2 + 40 + 4) + sizeof(int) * (2 + nloc + 2);
+}
+
+template <int CS>
+cudaError_t launch_pqr_cluster_cs(double *M, int64_t mstride, int n, double *tau, int *piv,
+                                  int64_t vstride, const int *active, int nshift, cudaStream_t st) {
+    const size_t smem = pqr_cluster_smem(n, CS);
+    cudaError_t e = smem_optin(pqr_cluster_kernel<CS>);
+    if (e != cudaSuccess) return e;
+    if (CS > 8) {
+        static std::once_flag once;
+        std::call_once(once, [] {
+            cudaFuncSetAttribute(pqr_cluster_kernel<CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        });
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CS, nshift, 1);
+    cfg.blockDim = dim3(PQRC_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, pqr_cluster_kernel<CS>, M, mstride, n, tau, piv, vstride, active);
+}
+
+}  // namespace
+
+// cluster size for an n x n Gram matrix (0: too large for distributed shared memory)
+int pqr_cluster_size(int n) {
+    const size_t cap = 220 * 1024;
+    if (pqr_cluster_smem(n, 8) <= cap) return 8;
+    if (pqr_cluster_smem(n, 16) <= cap) return 16;
+    return 0;
+}
+
+cudaError_t launch_pqr_cluster(double *M, int64_t mstride, int n, double *tau, int *piv,
+                               int64_t vstride, const int *active, int nshift, cudaStream_t st) {
+    if (nshift <= 0 || n <= 0) return cudaSuccess;
+    const int cs = pqr_cluster_size(n);
+    if (cs == 8) return launch_pqr_cluster_cs<8>(M, mstride, n, tau, piv, vstride, active, nshift, st);
+    if (cs == 16) return launch_pqr_cluster_cs<16>(M, mstride, n, tau, piv, vstride, active, nshift, st);
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_form_q_rows(const double *V, int64_t vstride, int n, const double *tau,
+                               int64_t tstride, double *QT, int64_t qstride, const int *active,
+                               int nshift, cudaStream_t st) {
+    if (nshift <= 0 || n <= 0) return cudaSuccess;
+    const size_t smem = sizeof(double) * FQ_WARPS * (size_t)n;
+    cudaError_t e = smem_optin(form_q_rows_kernel);
+    if (e != cudaSuccess) return e;
+    dim3 grid((n + FQ_WARPS - 1) / FQ_WARPS, nshift);
+    form_q_rows_kernel<<<grid, FQ_WARPS * 32, smem, st>>>(V, vstride, n, tau, tstride, QT, qstride,
+                                                         active);
+    return cudaGetLastError();
+}
+
+namespace {
 }  // namespace
 
 cudaError_t launch_pqr(double *GT, int64_t gstride, int c, int nR, int ldg, double *tau, int *piv,
