@@ -98,6 +98,17 @@ int copy_tiles(int rows, int cols);
 void launch_copy_prefixed(const CopyTask *dev_tasks, const int *dev_prefix, int ntasks,
                           int total_tiles, int nshift, const double *mu, cudaStream_t st);
 
+// target of one segment pair (a <= b) of the symmetric Schur update: element
+// (ra, cb) lives at base + z*bs + (trans ? cb*ldc + ra : ra*ldc + cb)
+struct SchurTarget {
+    double *base;
+    int64_t bs;
+    int ldc, trans;
+};
+int schur_sym_tiles(int R);
+void launch_schur_sym(const double *X, const double *Bg, int64_t sx, int ld, int R, int K,
+                      const int *seg_of, const int *seg_start, int nseg, const SchurTarget *tbl,
+                      int nshift, cudaStream_t st);
 int gemm_tiles(int M, int N);
 void launch_gemm(const GemmTask *dev_tasks, const int *dev_tile_prefix, int ntasks,
                  int total_tiles, int nshift, cudaStream_t st, bool schur = false,

@@ -286,7 +286,12 @@ private:
     int *d_status_ = nullptr, *d_rank_ = nullptr;
     std::vector<Cl> cl_;
     std::vector<Blk> diag_;
-    std::vector<int> tile_map_;
+    std::vector<int> tile_map_, seg_of_, seg_start_;
+    std::vector<SchurTarget> schur_tbl_;
+    static bool schur_pairs_mode() {
+        static const bool on = getenv("H2L_SCHUR_PAIRS") != nullptr;
+        return on;
+    }
     std::vector<char> elim_, pend_diag_;
     std::set<Pair> pend_off_;
     std::map<Pair, Blk> offd_, coup_, fill_;
@@ -348,6 +353,8 @@ private:
             snprintf(key, sizeof key, "M<=%d N<=%d K<=%d", bucket(t.M), bucket(t.N), bucket(t.K));
             ghist_[key] += 2.0 * t.M * t.N * (double)t.K * s_;
         }
+        for (auto &t : b.t)
+            ghist_["#padded flops"] += 2.0 * ((t.M + 63) / 64 * 64) * ((t.N + 63) / 64 * 64) * (double)t.K * s_;
         ghist_["#launch tiles"] += b.tiles;
         ghist_["#launches"] += 1;
     }
@@ -357,8 +364,8 @@ private:
         double tot = 0;
         for (auto &kv : ghist_) if (kv.first[0] != '#') { v.push_back({kv.second, kv.first}); tot += kv.second; }
         std::sort(v.rbegin(), v.rend());
-        fprintf(stderr, "schur gemm: %.3g flops, %.0f launches, %.0f tiles (per shift-row)\n", tot,
-                ghist_["#launches"], ghist_["#launch tiles"]);
+        fprintf(stderr, "schur gemm: %.3g flops (%.3g tile-padded), %.0f launches, %.0f tiles (per shift-row)\n",
+                tot, ghist_["#padded flops"], ghist_["#launches"], ghist_["#launch tiles"]);
         for (size_t q = 0; q < v.size() && q < 25; ++q)
             fprintf(stderr, "  %-28s %5.1f%%\n", v[q].second.c_str(), 100.0 * v[q].first / tot);
         ghist_.clear();
@@ -1150,46 +1157,25 @@ private:
                             0.0), s_);
             flush(g0, s_);
             Blk Xb = alloc(R, nR, false);
-            GemmBatch g1;
-            for (auto &sg : segs) {
-                if (sg.len <= 0) continue;
-                const double *A; int lda, tA;
-                seg_as_A(sg, &A, &lda, &tA);
-                add_gemm(g1, gm(A, sg.ss, lda, tA, G.p, G.bs, nR, 0, Xb.at(sg.row, 0), Xb.bs, nR,
-                                sg.len, nR, nR, 1.0, 0.0), s_);
-            }
-            flush(g1, s_);
-            // algorithmic panel work (survey §8d): TRSM R nR^2 + D-scale R nR
-            flops += (double)R * nR * nR + (double)R * nR;
-            // ---- K6: Schur updates of every target pair, one grouped launch
-            GemmBatch g;
-            double sch = 0.0, sch_bytes = 16.0 * (double)R * nR;  // X and W read once
-            auto upd = [&](const Seg &a, const Seg &b, double *C, int64_t sC, int ldc) {
-                if (a.len <= 0 || b.len <= 0) return;
-                const double *B; int ldb, tB;
-                seg_as_Bt(b, &B, &ldb, &tB);
-                add_gemm(g, gm(Xb.at(a.row, 0), Xb.bs, nR, 0, B, b.ss, ldb, tB, C, sC, ldc, a.len,
-                               b.len, nR, -1.0, 1.0), s_);
-                sch += (a.who == b.who ? 1.0 : 2.0) * (double)a.len * b.len * nR;
-                sch_bytes += 16.0 * (double)a.len * b.len;  // target read + write
-            };
-            upd(segs[0], segs[0], D.at(nR, nR), D.bs, m);
-            for (size_t x = 1; x < segs.size(); ++x) {
-                const Seg &sj = segs[x];
-                const int j = sj.who;
-                Blk &Dj = diag_[j];
-                upd(sj, sj, Dj.at(sj.lo, sj.lo), Dj.bs, Dj.cols);
-                if (i < j) {
-                    Blk &O = offd_.at({i, j});
-                    upd(segs[0], sj, O.at(nR, sj.lo), O.bs, O.cols);
+            // target block of a segment pair (x <= y); creates fill blocks (gldl.py:398-409)
+            auto target = [&](size_t x, size_t y, double **C, int64_t *sC, int *ldc, int *trans) {
+                const Seg &a = segs[x], &b = segs[y];
+                *trans = 0;
+                if (x == 0 && y == 0) {
+                    *C = D.at(nR, nR); *sC = D.bs; *ldc = m;
+                } else if (x == y) {
+                    Blk &Dj = diag_[a.who];
+                    *C = Dj.at(a.lo, a.lo); *sC = Dj.bs; *ldc = Dj.cols;
+                } else if (x == 0) {
+                    const int j = b.who;
+                    if (i < j) {
+                        Blk &O = offd_.at({i, j});
+                        *C = O.at(nR, b.lo); *sC = O.bs; *ldc = O.cols;
+                    } else {
+                        Blk &O = offd_.at({j, i});
+                        *C = O.at(b.lo, nR); *sC = O.bs; *ldc = O.cols; *trans = 1;
+                    }
                 } else {
-                    Blk &O = offd_.at({j, i});
-                    upd(sj, segs[0], O.at(sj.lo, nR), O.bs, O.cols);
-                }
-            }
-            for (size_t x = 1; x < segs.size(); ++x)
-                for (size_t y = x + 1; y < segs.size(); ++y) {
-                    const Seg &a = segs[x], &b = segs[y];
                     const Pair key{a.who, b.who};
                     Blk *T;
                     auto o = offd_.find(key);
@@ -1206,12 +1192,94 @@ private:
                         }
                         T = &f->second;
                     }
-                    upd(a, b, T->at(a.lo, b.lo), T->bs, T->cols);
+                    *C = T->at(a.lo, b.lo); *sC = T->bs; *ldc = T->cols;
                 }
+            };
+            double sch = 0.0, sch_bytes = 16.0 * (double)R * nR;  // X and W read once
+            for (size_t x = 0; x < segs.size(); ++x)
+                for (size_t y = x; y < segs.size(); ++y) {
+                    if (segs[x].len <= 0 || segs[y].len <= 0) continue;
+                    sch += (x == y ? 1.0 : 2.0) * (double)segs[x].len * segs[y].len * nR;
+                    sch_bytes += 16.0 * (double)segs[x].len * segs[y].len;  // target r + w
+                }
+            if (!schur_pairs_mode()) {
+                // ---- K5/K6: gather the panel rows Bg = [B_0; B_1; ...] (R x nR), one GEMM
+                // X = Bg G, then the symmetric update C_big -= X Bg^T over the upper
+                // triangle of the R x R panel space, scattered to the target blocks
+                Blk Bg = alloc(R, nR, false);
+                CopyBatch gc;
+                for (auto &sg : segs) {
+                    if (sg.len <= 0) continue;
+                    const double *A; int lda, tA;
+                    seg_as_A(sg, &A, &lda, &tA);
+                    add_copy(gc, cp(A, sg.ss, lda, Bg.at(sg.row, 0), Bg.bs, nR, sg.len, nR, tA));
+                }
+                flush(gc);
+                GemmBatch g1;
+                add_gemm(g1, gm(Bg.p, Bg.bs, nR, 0, G.p, G.bs, nR, 0, Xb.p, Xb.bs, nR, R, nR, nR,
+                                1.0, 0.0), s_);
+                flush(g1, s_);
+                const int ns = (int)segs.size();
+                seg_of_.assign(R, 0);
+                seg_start_.assign(ns, 0);
+                schur_tbl_.assign((size_t)ns * ns, SchurTarget{nullptr, 0, 0, 0});
+                for (int x = 0; x < ns; ++x) {
+                    seg_start_[x] = segs[x].row;
+                    for (int r = 0; r < segs[x].len; ++r) seg_of_[segs[x].row + r] = x;
+                }
+                for (int x = 0; x < ns; ++x)
+                    for (int y = x; y < ns; ++y) {
+                        if (segs[x].len <= 0 || segs[y].len <= 0) continue;
+                        SchurTarget &e = schur_tbl_[(size_t)x * ns + y];
+                        target(x, y, &e.base, &e.bs, &e.ldc, &e.trans);
+                    }
+                const int *d_seg = (const int *)stage(seg_of_.data(), sizeof(int) * R);
+                const int *d_start = (const int *)stage(seg_start_.data(), sizeof(int) * ns);
+                const SchurTarget *d_tbl = (const SchurTarget *)stage(
+                    schur_tbl_.data(), sizeof(SchurTarget) * schur_tbl_.size());
+                {
+                    Timed tm(this, 1);
+                    launch_schur_sym(Xb.p, Bg.p, Xb.bs, nR, R, nR, d_seg, d_start, ns, d_tbl, s_,
+                                     st_);
+                }
+                CK(cudaGetLastError());
+                dbg_sync("schur-sym");
+                st_acc_->launches++;
+                st_acc_->gemm_flops_exec += 2.0 * (double)schur_sym_tiles(R) * 64 * 64 * nR * s_;
+                release(Bg);
+                // algorithmic panel work (survey §8d): TRSM R nR^2 + D-scale R nR
+                flops += (double)R * nR * nR + (double)R * nR;
+            } else {
+            GemmBatch g1;
+            for (auto &sg : segs) {
+                if (sg.len <= 0) continue;
+                const double *A; int lda, tA;
+                seg_as_A(sg, &A, &lda, &tA);
+                add_gemm(g1, gm(A, sg.ss, lda, tA, G.p, G.bs, nR, 0, Xb.at(sg.row, 0), Xb.bs, nR,
+                                sg.len, nR, nR, 1.0, 0.0), s_);
+            }
+            flush(g1, s_);
+            // algorithmic panel work (survey §8d): TRSM R nR^2 + D-scale R nR
+            flops += (double)R * nR * nR + (double)R * nR;
+            // ---- K6 (H2L_SCHUR_PAIRS=1): one grouped launch of per-pair GEMM tasks
+            GemmBatch g;
+            for (size_t x = 0; x < segs.size(); ++x)
+                for (size_t y = x; y < segs.size(); ++y) {
+                    const Seg &a = segs[x], &b = segs[y];
+                    if (a.len <= 0 || b.len <= 0) continue;
+                    double *C; int64_t sC; int ldc, trans;
+                    target(x, y, &C, &sC, &ldc, &trans);
+                    const Seg &ra = trans ? b : a, &cb = trans ? a : b;
+                    const double *B; int ldb, tB;
+                    seg_as_Bt(cb, &B, &ldb, &tB);
+                    add_gemm(g, gm(Xb.at(ra.row, 0), Xb.bs, nR, 0, B, cb.ss, ldb, tB, C, sC, ldc,
+                                   ra.len, cb.len, nR, -1.0, 1.0), s_);
+                }
+            flush(g, s_, 1);
+            }
             flops += sch;
             st_acc_->schur_flops += sch * s_;
             st_acc_->bytes += sch_bytes * s_;
-            flush(g, s_, 1);
             release(WI);
             release(XI);
             release(G);

@@ -114,15 +114,72 @@ struct Loader {
     }
 };
 
+// K loop of one BM x BN tile: acc += op(A)[m0:, :] op(B)[:, n0:] (cp.async
+// pipeline, DMMA.8x8x4).  Shared by the grouped GEMM and the Schur kernel.
+template <class Cfg>
+__device__ __forceinline__ void tile_mainloop(const double *A, int lda, int tA, int M,
+                                              const double *B, int ldb, int b_trans, int N, int K,
+                                              int m0, int n0, int wm, int wn,
+                                              double (&acc)[Cfg::FM][Cfg::FN][2]) {
+    constexpr int BM = Cfg::BM, BN = Cfg::BN, STAGES = Cfg::STAGES, FM = Cfg::FM, FN = Cfg::FN;
+    constexpr int BK = Cfg::BK, SK = Cfg::SK, THREADS = Cfg::THREADS;
+    extern __shared__ __align__(16) double gsm[];
+    double (*As)[BM][SK] = reinterpret_cast<double (*)[BM][SK]>(gsm);
+    double (*Bs)[BN][SK] = reinterpret_cast<double (*)[BN][SK]>(gsm + STAGES * BM * SK);
+    const int tid = threadIdx.x, lane = tid & 31;
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const int nk = (K + BK - 1) / BK;
+    const Loader<BM, THREADS, BK, SK> la(A, lda, tA, M, m0, tid);
+    const Loader<BN, THREADS, BK, SK> lb(B, ldb, b_trans, N, n0, tid);
+    const unsigned sA = (unsigned)__cvta_generic_to_shared(&As[0][0][0]);
+    const unsigned sB = (unsigned)__cvta_generic_to_shared(&Bs[0][0][0]);
+    constexpr unsigned SA_STAGE = BM * SK * sizeof(double), SB_STAGE = BN * SK * sizeof(double);
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < nk) {
+            la.load(sA + s * SA_STAGE, s, K);
+            lb.load(sB + s * SB_STAGE, s, K);
+        }
+        cp_commit();
+    }
+    for (int kc = 0; kc < nk; ++kc) {
+        cp_wait<STAGES - 2>();
+        __syncthreads();
+        const int nxt = kc + STAGES - 1;
+        if (nxt < nk) {
+            const int sl = nxt % STAGES;
+            la.load(sA + sl * SA_STAGE, nxt, K);
+            lb.load(sB + sl * SB_STAGE, nxt, K);
+        }
+        cp_commit();
+        const int cur = kc % STAGES;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double af[FM], bf[FN];
+#pragma unroll
+            for (int i = 0; i < FM; ++i) af[i] = As[cur][wm + i * 8 + (lane >> 2)][kk + (lane & 3)];
+#pragma unroll
+            for (int j = 0; j < FN; ++j) bf[j] = Bs[cur][wn + j * 8 + (lane >> 2)][kk + (lane & 3)];
+#pragma unroll
+            for (int i = 0; i < FM; ++i)
+#pragma unroll
+                for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+    }
+    cp_wait<0>();
+    __syncthreads();
+}
+
 template <class Cfg>
 __device__ __forceinline__ void gemm_body(const GemmTask *tasks, const int *prefix, int ntasks,
                                           const int *tile_task) {
     constexpr int BM = Cfg::BM, BN = Cfg::BN, STAGES = Cfg::STAGES, FM = Cfg::FM, FN = Cfg::FN;
-    constexpr int BK = Cfg::BK, SK = Cfg::SK;
+    constexpr int SK = Cfg::SK;
     constexpr int THREADS = Cfg::THREADS, CS = Cfg::CS;
     extern __shared__ __align__(16) double gsm[];
-    double (*As)[BM][SK] = reinterpret_cast<double (*)[BM][SK]>(gsm);
-    double (*Bs)[BN][SK] = reinterpret_cast<double (*)[BN][SK]>(gsm + STAGES * BM * SK);
     double *Cs = gsm + STAGES * (BM + BN) * SK;
 
     // tile -> task: one load from the staged map (large launches) or a binary
@@ -157,51 +214,7 @@ __device__ __forceinline__ void gemm_body(const GemmTask *tasks, const int *pref
     cp_commit();
 
     double acc[FM][FN][2];
-#pragma unroll
-    for (int i = 0; i < FM; ++i)
-#pragma unroll
-        for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-    const int nk = (tk.K + BK - 1) / BK;
-    const Loader<BM, THREADS, BK, SK> la(A, tk.lda, tk.tA, tk.M, m0, tid);
-    const Loader<BN, THREADS, BK, SK> lb(B, tk.ldb, b_trans, tk.N, n0, tid);
-    const unsigned sA = (unsigned)__cvta_generic_to_shared(&As[0][0][0]);
-    const unsigned sB = (unsigned)__cvta_generic_to_shared(&Bs[0][0][0]);
-    constexpr unsigned SA_STAGE = BM * SK * sizeof(double), SB_STAGE = BN * SK * sizeof(double);
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-        if (s < nk) {
-            la.load(sA + s * SA_STAGE, s, tk.K);
-            lb.load(sB + s * SB_STAGE, s, tk.K);
-        }
-        cp_commit();
-    }
-    for (int kc = 0; kc < nk; ++kc) {
-        cp_wait<STAGES - 2>();
-        __syncthreads();
-        const int nxt = kc + STAGES - 1;
-        if (nxt < nk) {
-            const int sl = nxt % STAGES;
-            la.load(sA + sl * SA_STAGE, nxt, tk.K);
-            lb.load(sB + sl * SB_STAGE, nxt, tk.K);
-        }
-        cp_commit();
-        const int cur = kc % STAGES;
-#pragma unroll
-        for (int kk = 0; kk < BK; kk += 4) {
-            double af[FM], bf[FN];
-#pragma unroll
-            for (int i = 0; i < FM; ++i) af[i] = As[cur][wm + i * 8 + (lane >> 2)][kk + (lane & 3)];
-#pragma unroll
-            for (int j = 0; j < FN; ++j) bf[j] = Bs[cur][wn + j * 8 + (lane >> 2)][kk + (lane & 3)];
-#pragma unroll
-            for (int i = 0; i < FM; ++i)
-#pragma unroll
-                for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-        }
-    }
-    cp_wait<0>();
-    __syncthreads();
+    tile_mainloop<Cfg>(A, tk.lda, tk.tA, tk.M, B, tk.ldb, b_trans, tk.N, tk.K, m0, n0, wm, wn, acc);
 
     // epilogue: C = alpha*acc + beta*C
     if (Cfg::CSTAGE) {
@@ -245,6 +258,114 @@ __device__ __forceinline__ void gemm_body(const GemmTask *tasks, const int *pref
     }
 }
 
+// K6 as one symmetric update per elimination step (engine.cu eliminate):
+// C_big -= X Bg^T over the upper triangle of the R x R panel space, where X
+// (R x K) and Bg (R x K) are the panel's rows stacked segment by segment.
+// Tiles never straddle tasks, so no tile is padded except at the end of R (the
+// per-pair task list padded every segment to a multiple of 64); the epilogue
+// scatters element (r, c), r <= c, to its target block through the
+// segment-pair table (diagonal segments also write the mirrored element).
+template <class Cfg>
+__device__ __forceinline__ void schur_sym_body(const double *X, const double *Bg, int64_t sx,
+                                               int ld, int R, int K, const int *seg_of,
+                                               const int *seg_start, int nseg,
+                                               const SchurTarget *tbl) {
+    constexpr int BM = Cfg::BM, BN = Cfg::BN, FM = Cfg::FM, FN = Cfg::FN;
+    static_assert(BM == BN, "square tiles");
+    // upper-triangular tile index -> (I <= J)
+    const int t = blockIdx.x;
+    int J = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((J + 1) * (J + 2) / 2 <= t) ++J;
+    while (J * (J + 1) / 2 > t) --J;
+    const int I = t - J * (J + 1) / 2;
+    const int m0 = I * BM, n0 = J * BN;
+    const int z = blockIdx.y;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int WCOLS = BN / Cfg::WN;
+    const int wm = (warp / WCOLS) * Cfg::WM, wn = (warp % WCOLS) * Cfg::WN;
+    double acc[FM][FN][2];
+    tile_mainloop<Cfg>(X + z * sx, ld, 0, R, Bg + z * sx, ld, 0, R, K, m0, n0, wm, wn, acc);
+    // epilogue: the tile's row / column segments and the few segment-pair targets
+    // it touches are resolved once into shared memory; then, like the grouped
+    // GEMM, all target loads of a fragment row are issued before its stores
+    constexpr int MAXT = 64;
+    __shared__ int s_rseg[BM], s_roff[BM], s_cseg[BN], s_coff[BN], s_box[4];
+    __shared__ SchurTarget s_tbl[MAXT];
+
+    for (int q = tid; q < BM + BN; q += Cfg::THREADS) {
+        const int x = q < BM ? m0 + q : n0 + (q - BM);
+        const int sg = x < R ? seg_of[x] : -1;
+        const int off = sg >= 0 ? x - seg_start[sg] : 0;
+        if (q < BM) { s_rseg[q] = sg; s_roff[q] = off; }
+        else { s_cseg[q - BM] = sg; s_coff[q - BM] = off; }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const int rl = min(BM, R - m0) - 1, cl = min(BN, R - n0) - 1;
+        s_box[0] = s_rseg[0];
+        s_box[1] = s_rseg[rl] - s_rseg[0] + 1;
+        s_box[2] = s_cseg[0];
+        s_box[3] = s_cseg[cl] - s_cseg[0] + 1;
+    }
+    __syncthreads();
+    const int alo = s_box[0], na = s_box[1], blo = s_box[2], nb = s_box[3];
+    const bool in_smem = na * nb <= MAXT;
+    if (in_smem)
+        for (int q = tid; q < na * nb; q += Cfg::THREADS)
+            s_tbl[q] = tbl[(size_t)(alo + q / nb) * nseg + blo + q % nb];
+    __syncthreads();
+    auto entry = [&](int a, int b) -> SchurTarget {
+        return in_smem ? s_tbl[(a - alo) * nb + (b - blo)] : tbl[(size_t)a * nseg + b];
+    };
+#pragma unroll
+    for (int i = 0; i < FM; ++i) {
+        const int rl = wm + i * 8 + (lane >> 2);
+        const int r = m0 + rl, a = s_rseg[rl], ra = s_roff[rl];
+        if (a < 0) continue;
+        double *ptr[FN][2];
+        double cv[FN][2];
+#pragma unroll
+        for (int j = 0; j < FN; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int cl = wn + j * 8 + 2 * (lane & 3) + h;
+                const int b = s_cseg[cl], cb = s_coff[cl];
+                ptr[j][h] = nullptr;
+                cv[j][h] = 0.0;
+                if (b < 0 || n0 + cl < r) continue;
+                const SchurTarget e = entry(a, b);
+                if (!e.base) continue;
+                double *p = e.base + z * e.bs + (e.trans ? (int64_t)cb * e.ldc + ra
+                                                          : (int64_t)ra * e.ldc + cb);
+                ptr[j][h] = p;
+                cv[j][h] = *p;
+            }
+#pragma unroll
+        for (int j = 0; j < FN; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                if (ptr[j][h]) *ptr[j][h] = cv[j][h] - acc[i][j][h];
+    }
+    // diagonal segment pairs: the mirrored element (a separate, rare pass)
+#pragma unroll
+    for (int i = 0; i < FM; ++i) {
+        const int rl = wm + i * 8 + (lane >> 2);
+        const int r = m0 + rl, a = s_rseg[rl], ra = s_roff[rl];
+        if (a < 0) continue;
+#pragma unroll
+        for (int j = 0; j < FN; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int cl = wn + j * 8 + 2 * (lane & 3) + h;
+                const int b = s_cseg[cl], cb = s_coff[cl];
+                if (b != a || cb == ra || n0 + cl < r) continue;
+                const SchurTarget e = entry(a, b);
+                if (!e.base) continue;
+                e.base[z * e.bs + (int64_t)cb * e.ldc + ra] -= acc[i][j][h];
+            }
+    }
+}
+
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_kernel(const GemmTask *tasks,
                                                             const int *prefix, int ntasks,
@@ -257,6 +378,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) schur_gemm_kernel(con
                                                                   const int *prefix, int ntasks,
                                                             const int *tile_task) {
     gemm_body<Cfg>(tasks, prefix, ntasks, tile_task);
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) schur_sym_kernel(
+    const double *X, const double *Bg, int64_t sx, int ld, int R, int K, const int *seg_of,
+    const int *seg_start, int nseg, const SchurTarget *tbl) {
+    schur_sym_body<Cfg>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl);
 }
 
 // production configuration (chosen with tools/gemm_bench.py)
@@ -272,6 +400,22 @@ void launch_cfg(const GemmTask *dev_tasks, const int *dev_tile_prefix, int ntask
 }
 
 }  // namespace
+
+int schur_sym_tiles(int R) {
+    const int nt = (R + Prod::BM - 1) / Prod::BM;
+    return nt * (nt + 1) / 2;
+}
+
+void launch_schur_sym(const double *X, const double *Bg, int64_t sx, int ld, int R, int K,
+                      const int *seg_of, const int *seg_start, int nseg, const SchurTarget *tbl,
+                      int nshift, cudaStream_t st) {
+    const int tiles = schur_sym_tiles(R);
+    if (tiles <= 0 || nshift <= 0 || K <= 0) return;
+    smem_optin(schur_sym_kernel<Prod>);
+    dim3 grid(tiles, nshift);
+    schur_sym_kernel<Prod><<<grid, Prod::THREADS, Prod::SMEM, st>>>(X, Bg, sx, ld, R, K, seg_of,
+                                                                     seg_start, nseg, tbl);
+}
 
 int gemm_tiles(int M, int N) {
     if (M <= 0 || N <= 0) return 0;
