@@ -10,7 +10,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libh2ldl.so")
-SOURCES = ["engine.cu", "k_copy.cu", "k_gemm.cu", "k_bk.cu", "k_panel.cu", "k_qr.cu", "k_rrqr.cu"]
+SOURCES = ["engine.cu", "k_copy.cu", "k_gemm.cu", "k_bk.cu", "k_panel.cu", "k_qr.cu", "k_rrqr.cu", "k_bk_cluster.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-shared", "-Xcompiler", "-O2"]

@@ -114,6 +114,10 @@ void launch_gemm(const GemmTask *dev_tasks, const int *dev_tile_prefix, int ntas
                  int total_tiles, int nshift, cudaStream_t st, bool schur = false,
                  const int *dev_tile_task = nullptr);
 
+// cluster BK for fronts above the single-CTA shared-memory size (k_bk_cluster.cu)
+int bk_cluster_size(int n);
+cudaError_t launch_bk_cluster(const BkJob *dev_jobs, int njobs, int nshift, int n, int64_t *counts,
+                              int *status, cudaStream_t st);
 int64_t bk_scratch_doubles(int n);
 cudaError_t launch_bk_engine(const BkJob *dev_jobs, int njobs, int nshift, int nmax,
                              int64_t *counts, int *status, double *scratch,

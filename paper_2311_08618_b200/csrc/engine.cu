@@ -288,6 +288,10 @@ private:
     std::vector<Blk> diag_;
     std::vector<int> tile_map_, seg_of_, seg_start_;
     std::vector<SchurTarget> schur_tbl_;
+    static bool bk_single_mode() {
+        static const bool on = getenv("H2L_BK_SINGLE") != nullptr;
+        return on;
+    }
     static bool schur_pairs_mode() {
         static const bool on = getenv("H2L_SCHUR_PAIRS") != nullptr;
         return on;
@@ -395,7 +399,7 @@ private:
         stage_.off = 0;
     }
     // H2L_HOSTPROF: host time blocked in stream syncs vs the wave's wall time
-    double wait_ms_ = 0.0;
+    double wait_ms_ = 0.0, host_rec_ms_ = 0.0, host_elim_ms_ = 0.0;
     static bool hostprof_on() {
         static const bool on = getenv("H2L_HOSTPROF") != nullptr;
         return on;
@@ -613,7 +617,7 @@ private:
     // ------------------------------------------------------------------ wave
     void run_wave(const double *mu, int s, int64_t *counts, int32_t *status, h2l_stats &acc) {
         const auto wall0 = std::chrono::steady_clock::now();
-        wait_ms_ = 0.0;
+        wait_ms_ = host_rec_ms_ = host_elim_ms_ = 0.0;
         s_ = s;
         st_acc_ = &acc;
         ev_used_ = 0;
@@ -690,9 +694,10 @@ private:
         CK(cudaFreeAsync(d_rank_, st_));
         sync();
         if (hostprof_on())
-            fprintf(stderr, "hostprof: wave of %d shifts: wall %.1f ms, blocked in syncs %.1f ms\n", s,
+            fprintf(stderr, "hostprof: wave of %d shifts: wall %.1f ms, blocked in syncs %.1f ms, "
+                    "host in recompress %.1f ms (incl. syncs), in eliminate %.1f ms\n", s,
                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count(),
-                    wait_ms_);
+                    wait_ms_, host_rec_ms_, host_elim_ms_);
         st_acc_ = nullptr;
     }
 
@@ -808,8 +813,13 @@ private:
         for (int i = 0; i < nc; ++i) {
             if (cl_[i].m == 0) continue;
             if (leaf) ensure_front(i);
+            const auto h0 = std::chrono::steady_clock::now();
             recompress(i);
+            const auto h1 = std::chrono::steady_clock::now();
             eliminate(i);
+            const auto h2 = std::chrono::steady_clock::now();
+            host_rec_ms_ += std::chrono::duration<double, std::milli>(h1 - h0).count();
+            host_elim_ms_ += std::chrono::duration<double, std::milli>(h2 - h1).count();
             if ((i & (nc / 8 - 1)) == 0 && nc >= 8) memtrace("cluster", i);
         }
         if (leaf) ensure_all();
@@ -1329,6 +1339,17 @@ private:
     void bk_launch(double *a, int64_t astride, int ld, int n, int *perm, double *dinfo, int64_t ps) {
         BkJob jb{a, astride, ld, n, perm, dinfo, ps};
         const BkJob *dj = (const BkJob *)stage(&jb, sizeof(jb));
+        // fronts beyond one CTA's shared memory: the cluster kernel keeps the packed
+        // triangle in distributed shared memory (same arithmetic, bit-identical)
+        if (bk_scratch_doubles(n) && bk_cluster_size(n) && !bk_single_mode()) {
+            {
+                Timed tm(this, 3);
+                CK(launch_bk_cluster(dj, 1, s_, n, d_counts_, d_status_, st_));
+            }
+            dbg_sync("bk-cluster");
+            st_acc_->launches++;
+            return;
+        }
         const int64_t scr = bk_scratch_doubles(n);
         double *scratch = nullptr;
         if (scr) CK(cudaMallocFromPoolAsync((void **)&scratch, sizeof(double) * scr * s_, pool_, st_));
@@ -1948,6 +1969,48 @@ __global__ void naive_gemm_kernel(const GemmTask *tasks, int ntasks) {
     }
 }
 }  // namespace h2l
+
+// engine-mode BK of `count` n x n row-major matrices (host), single-CTA (mode 0)
+// or cluster (mode 1) kernel: factor (lower triangle), perm, dinfo, counts, status
+extern "C" int h2l_internal_bk_engine(int device, int mode, int n, int count, double *a, int *perm,
+                                      double *dinfo, int64_t *counts, int *status) {
+    return guarded(nullptr, [&] {
+        CK(cudaSetDevice(device));
+        const int64_t nn = (int64_t)n * n, ps = n;
+        double *da, *dd, *scr = nullptr;
+        int *dp, *dst;
+        int64_t *dc;
+        h2l::BkJob *dj;
+        CK(cudaMalloc(&da, sizeof(double) * nn * count));
+        CK(cudaMalloc(&dd, sizeof(double) * 3 * ps * count));
+        CK(cudaMalloc(&dp, sizeof(int) * ps * count));
+        CK(cudaMalloc(&dst, sizeof(int) * count));
+        CK(cudaMalloc(&dc, sizeof(int64_t) * 3 * count));
+        CK(cudaMalloc(&dj, sizeof(h2l::BkJob)));
+        CK(cudaMemcpy(da, a, sizeof(double) * nn * count, cudaMemcpyHostToDevice));
+        CK(cudaMemset(dst, 0, sizeof(int) * count));
+        CK(cudaMemset(dc, 0, sizeof(int64_t) * 3 * count));
+        h2l::BkJob jb{da, nn, n, n, dp, dd, ps};
+        CK(cudaMemcpy(dj, &jb, sizeof(jb), cudaMemcpyHostToDevice));
+        if (mode == 1) {
+            if (!h2l::bk_cluster_size(n)) throw h2l::CudaFail(H2L_EINVAL, "n too large for the cluster BK");
+            CK(h2l::launch_bk_cluster(dj, 1, count, n, dc, dst, 0));
+        } else {
+            const int64_t sd = h2l::bk_scratch_doubles(n);
+            if (sd) CK(cudaMalloc(&scr, sizeof(double) * sd * count));
+            CK(h2l::launch_bk_engine(dj, 1, count, n, dc, dst, scr, sd, 0));
+        }
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpy(a, da, sizeof(double) * nn * count, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(perm, dp, sizeof(int) * ps * count, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(dinfo, dd, sizeof(double) * 3 * ps * count, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(counts, dc, sizeof(int64_t) * 3 * count, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(status, dst, sizeof(int) * count, cudaMemcpyDeviceToHost));
+        for (void *p : {(void *)da, (void *)dd, (void *)dp, (void *)dst, (void *)dc, (void *)dj})
+            cudaFree(p);
+        if (scr) cudaFree(scr);
+    });
+}
 
 extern "C" int h2l_internal_gemm_check(int device, int M, int N, int K, int ntasks, int nshift,
                                        int reps, double *maxdiff_out) {

@@ -205,3 +205,38 @@ def test_engine_elimination_flops_match_oracle(name):
     _, _, st = ldl_counts_array(H, [mu])
     want = engine_ref.OracleEngine(H, mu, {}).run().elim_flops
     assert st["elim_flops"] == pytest.approx(want, rel=1e-12)
+
+
+@pytest.mark.parametrize("n", [232, 300, 417, 520])
+def test_cluster_bk_bit_identical_to_single_cta(n):
+    """The cluster BK (fronts above one CTA's shared memory) replays the single-CTA
+    kernel's arithmetic: factor, permutation, pivot blocks and counts bit-identical."""
+    import ctypes
+
+    lib = _native.load_library()
+    f = lib.h2l_internal_bk_engine
+    f.restype = ctypes.c_int
+    rng = np.random.default_rng(n)
+    count = 3
+    A = rng.standard_normal((count, n, n))
+    A = A + A.transpose(0, 2, 1)
+    A[1] += np.diag(np.linspace(-3, 3, n))
+    A[2, :, : n // 3] *= 1e-3  # scale spread: more row-max tests and 2x2 pivots
+    A[2, : n // 3, :] *= 1e-3
+    outs = []
+    for mode in (0, 1):
+        a = np.ascontiguousarray(A.copy())
+        perm = np.zeros((count, n), np.int32)
+        dinfo = np.zeros((count, 3 * n))
+        counts = np.zeros((count, 3), np.int64)
+        status = np.zeros(count, np.int32)
+        rc = f(0, mode, n, count, a.ctypes.data_as(ctypes.c_void_p), perm.ctypes.data_as(ctypes.c_void_p),
+               dinfo.ctypes.data_as(ctypes.c_void_p), counts.ctypes.data_as(ctypes.c_void_p),
+               status.ctypes.data_as(ctypes.c_void_p))
+        assert rc == 0
+        outs.append((np.tril(a), perm, dinfo, counts, status))
+    for x, y in zip(*outs):
+        assert np.array_equal(x, y)
+    w = [np.linalg.eigvalsh(A[q]) for q in range(count)]
+    assert [int(c[0]) for c in outs[1][3]] == [int(np.sum(v < 0)) for v in w]
+    assert (outs[0][2][:, 2::3] == 2.0).any()  # 2x2 pivots were exercised
