@@ -94,7 +94,10 @@ __global__ void __launch_bounds__(BKC_THREADS) bk_cluster_kernel(const BkJob *jo
     const int nwarp = nthr >> 5;
     const int nloc = (n - crank + CS - 1) / CS;  // own columns: crank, crank+CS, ...
     Dist<CS> A{bsm, n, crank};
-    const int64_t own = nloc > 0 ? A.off(crank + (nloc - 1) * CS) + (n - (crank + (nloc - 1) * CS)) : 0;
+    // the per-CTA buffers sit at the same offset in every CTA (remote w0/w1 reads):
+    // after the largest packed share, rank 0's
+    const int64_t l0 = (n + CS - 1) / CS - 1;
+    const int64_t own = l0 * n - (int64_t)CS * l0 * (l0 - 1) / 2 + (n - l0 * CS);
     double *pk = bsm + own;   // pivot column k (rows k..n-1 at index i)
     double *pk1 = pk + n;     // pivot column k+1
     double *w0 = pk1 + n;     // 2x2 L columns for own j
