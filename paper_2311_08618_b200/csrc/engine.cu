@@ -183,29 +183,57 @@ public:
             tot += pad4((int64_t)lsize(dense_[e].first) * lsize(dense_[e].second));
         }
         CK(cudaMalloc(&skel_, sizeof(double) * std::max<int64_t>(1, tot)));
-        double *tmp = nullptr;
-        int64_t tmpn = 0;
-        for (int i = 0; i < nleaf; ++i) tmpn = std::max<int64_t>(tmpn, (int64_t)lsize(i) * lsize(i));
-        for (auto &pr : dense_)
-            tmpn = std::max<int64_t>(tmpn, (int64_t)lsize(pr.first) * lsize(pr.second));
-        CK(cudaMalloc(&tmp, sizeof(double) * std::max<int64_t>(1, tmpn * 1)));
         skel_diag_.assign(nleaf, nullptr);
         skel_off_.clear();
-        // one block at a time (prologue runs once per H; simplicity over speed)
+        // batched congruences: up to CH blocks per pair of grouped GEMM launches
+        // (tmp_q = Q_a^T A_q, then S_q = tmp_q Q_b), identity bases as copies
+        struct Cg { const double *A; int ra, cb; const double *Qa, *Qb; double *C; };
+        std::vector<Cg> jobs;
         for (int i = 0; i < nleaf; ++i) {
-            const int m = lsize(i);
             skel_diag_[i] = skel_ + doff[i];
-            if (m == 0) continue;
-            const double *A = arena_ + pl->diag_off[i];
-            congruence(A, m, m, leaf_basis(i), leaf_basis(i), skel_diag_[i], tmp);
+            const int m = lsize(i);
+            if (m) jobs.push_back({arena_ + pl->diag_off[i], m, m, leaf_basis(i), leaf_basis(i), skel_diag_[i]});
         }
         for (size_t e = 0; e < dense_.size(); ++e) {
             const int i = dense_[e].first, j = dense_[e].second;
             double *dst = skel_ + ooff[e];
             skel_off_[dense_[e]] = dst;
-            congruence(arena_ + pl->dense_off[e], lsize(i), lsize(j), leaf_basis(i), leaf_basis(j),
-                       dst, tmp);
+            jobs.push_back({arena_ + pl->dense_off[e], lsize(i), lsize(j), leaf_basis(i), leaf_basis(j), dst});
         }
+        int64_t blk = 1;
+        for (auto &q : jobs) blk = std::max<int64_t>(blk, pad4((int64_t)q.ra * q.cb));
+        const int CH = (int)std::max<int64_t>(1, std::min<int64_t>(1024, (int64_t(1) << 28) / blk));
+        double *tmp = nullptr;
+        CK(cudaMalloc(&tmp, sizeof(double) * blk * std::min<size_t>(CH, jobs.size() + 1)));
+        const int s_save = s_;
+        s_ = 1;
+        for (size_t q0 = 0; q0 < jobs.size(); q0 += CH) {
+            const size_t q1 = std::min(jobs.size(), q0 + CH);
+            GemmBatch g1, g2;
+            CopyBatch c1, c2;
+            for (size_t q = q0; q < q1; ++q) {
+                const Cg &jb = jobs[q];
+                double *t = tmp + (int64_t)(q - q0) * blk;
+                const double *left = jb.A;
+                if (jb.Qa) {
+                    add_gemm(g1, gm(jb.Qa, 0, jb.ra, 1, jb.A, 0, jb.cb, 0, t, 0, jb.cb, jb.ra, jb.cb,
+                                    jb.ra, 1.0, 0.0), 1);
+                    left = t;
+                }
+                if (jb.Qb)
+                    add_gemm(g2, gm(left, 0, jb.cb, 0, jb.Qb, 0, jb.cb, 0, jb.C, 0, jb.cb, jb.ra, jb.cb,
+                                    jb.cb, 1.0, 0.0), 1);
+                else if (jb.Qa)
+                    add_copy(c2, cp(left, 0, jb.cb, jb.C, 0, jb.cb, jb.ra, jb.cb));
+                else
+                    add_copy(c1, cp(jb.A, 0, jb.cb, jb.C, 0, jb.cb, jb.ra, jb.cb));
+            }
+            flush(c1);
+            flush(g1, 1);
+            flush(g2, 1);
+            flush(c2);
+        }
+        s_ = s_save;
         CK(cudaStreamSynchronize(st_));
         stage_.off = 0;
         cudaFree(tmp);
@@ -582,35 +610,6 @@ private:
             if (on) cudaEventRecord(w->next_event(), w->st_);
         }
     };
-
-    // C (ra x cb) = Qa^T A Qb, Q == nullptr means identity (exact copy)
-    void congruence(const double *A, int ra, int cb, const double *Qa, const double *Qb,
-                    double *C, double *tmp) {
-        const int s_save = s_;
-        s_ = 1;
-        if (!Qa && !Qb) {
-            CopyBatch c;
-            add_copy(c, cp(A, 0, cb, C, 0, cb, ra, cb));
-            flush(c);
-        } else {
-            GemmBatch g;
-            const double *left = A;
-            if (Qa) {  // tmp = Qa^T A
-                add_gemm(g, gm(Qa, 0, ra, 1, A, 0, cb, 0, tmp, 0, cb, ra, cb, ra, 1.0, 0.0), 1);
-                flush(g, 1);
-                left = tmp;
-            }
-            if (Qb) {  // C = left Qb
-                add_gemm(g, gm(left, 0, cb, 0, Qb, 0, cb, 0, C, 0, cb, ra, cb, cb, 1.0, 0.0), 1);
-                flush(g, 1);
-            } else {
-                CopyBatch c;
-                add_copy(c, cp(left, 0, cb, C, 0, cb, ra, cb));
-                flush(c);
-            }
-        }
-        s_ = s_save;
-    }
 
     Blk &pair_block(std::map<Pair, Blk> &store, int a, int b) { return store[{a, b}]; }
 

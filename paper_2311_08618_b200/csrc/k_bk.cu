@@ -30,7 +30,7 @@
 namespace h2l {
 
 constexpr int BK_SMEM_MAX = 224;
-constexpr int BK_THREADS = 128;
+constexpr int BK_THREADS = 256;
 constexpr int BK_NMAX = 4096;
 
 namespace {

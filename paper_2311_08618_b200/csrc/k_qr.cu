@@ -254,6 +254,11 @@ __global__ void __launch_bounds__(PQRC_THREADS) pqr_cluster_kernel(double *Mg, i
                                                                    double *tau, int *piv,
                                                                    int64_t vstride,
                                                                    const int *active) {
+    // One cluster barrier per column: every CTA proposes its best unused column
+    // together with that column's Householder vector (double-buffered by step
+    // parity), then all CTAs take the same winner, copy its vector through
+    // DSMEM and apply it.  A CTA can run at most one step ahead of the slowest
+    // (it must pass the next barrier), so the two buffers never race.
     cg::cluster_group cluster = cg::this_cluster();
     const int crank = (int)cluster.block_rank();
     const int z = blockIdx.y;
@@ -261,19 +266,16 @@ __global__ void __launch_bounds__(PQRC_THREADS) pqr_cluster_kernel(double *Mg, i
     extern __shared__ __align__(16) double qsm[];
     const int nloc = (n + CS - 1) / CS;
     double *col = qsm;                          // [nloc][n]
-    double *vbuf = col + (size_t)nloc * n;      // [n]
-    double *nrm = vbuf + n;                     // [nloc]
-    double *slot_v = nrm + nloc;                // [1] candidate value
-    double *red = slot_v + 2;                   // [40]
-    double *hh = red + 40;                      // [4]: tau, scale, beta
-    int *slot_i = (int *)(hh + 4);              // [1] candidate index
-    int *usedl = slot_i + 2;                    // [nloc]
-    int *sp = usedl + nloc;                     // [1] pivot
+    double *vb = col + (size_t)nloc * n;        // [2][n] candidate vectors
+    double *vcur = vb + 2 * (size_t)n;          // [n] the step's reflector
+    double *nrm = vcur + n;                     // [nloc]
+    double *slot = nrm + nloc;                  // [2][4]: norm, tau, beta, (index as double)
+    double *red = slot + 8;                     // [32]: 16 values, then 16 ints
+    int *usedl = (int *)(red + 32);             // [nloc]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
     double *M = Mg + z * mstride;
     double *tz = tau + z * vstride;
     int *pz = piv + z * vstride;
-    // stage own columns (M symmetric: column q == row q, contiguous) and norms
     for (int lc = warp; lc < nloc; lc += nwarp) {
         const int q = lc * CS + crank;
         double s2 = 0.0;
@@ -289,8 +291,13 @@ __global__ void __launch_bounds__(PQRC_THREADS) pqr_cluster_kernel(double *Mg, i
         if (lane == 0) { nrm[lc] = s2; usedl[lc] = q < n ? 0 : 1; }
     }
     cluster.sync();  // every CTA has read M before any reflector overwrites it
+    __shared__ int s_lc, s_win[2];
+    __shared__ double s_tau;
     for (int j = 0; j < n; ++j) {
-        // ---- (1) local arg-max, published in the slot
+        const int par = j & 1;
+        double *myv = vb + (size_t)par * n;
+        double *mys = slot + 4 * par;
+        // ---- local candidate: arg-max of the unused trailing norms (lowest index on ties)
         double bv = -1.0;
         int bi = 0x7fffffff;
         for (int lc = tid; lc < nloc; lc += blockDim.x) {
@@ -305,89 +312,101 @@ __global__ void __launch_bounds__(PQRC_THREADS) pqr_cluster_kernel(double *Mg, i
             const int oi = __shfl_down_sync(0xffffffffu, bi, off);
             if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
         }
-        if (lane == 0) { red[warp] = bv; ((int *)(red + 20))[warp] = bi; }
+        if (lane == 0) { red[warp] = bv; ((int *)(red + 16))[warp] = bi; }
         __syncthreads();
         if (tid == 0) {
             double xv = red[0];
-            int xi = ((int *)(red + 20))[0];
+            int xi = ((int *)(red + 16))[0];
             for (int w = 1; w < nwarp; ++w) {
                 const double ov = red[w];
-                const int oi = ((int *)(red + 20))[w];
+                const int oi = ((int *)(red + 16))[w];
                 if (ov > xv || (ov == xv && oi < xi)) { xv = ov; xi = oi; }
             }
-            *slot_v = xv;
-            *slot_i = xi;
-        }
-        cluster.sync();
-        if (tid == 0) {
-            double xv = -1.0;
-            int xi = 0x7fffffff;
-            for (int c = 0; c < CS; ++c) {
-                const double ov = *cluster.map_shared_rank(slot_v, c);
-                const int oi = *cluster.map_shared_rank(slot_i, c);
-                if (ov > xv || (ov == xv && oi < xi)) { xv = ov; xi = oi; }
-            }
-            *sp = xi;
+            mys[0] = xv;
+            mys[3] = (double)xi;
+            s_lc = xi < n ? xi / CS : -1;
         }
         __syncthreads();
-        const int p = *sp;
-        const int owner = p % CS;
-        // ---- (2) Householder vector at the owner
-        if (owner == crank) {
-            double *x = col + (size_t)(p / CS) * n;
+        const int clc = s_lc;
+        // ---- its Householder vector (not applied unless it wins)
+        if (clc >= 0) {
+            const double *x = col + (size_t)clc * n;
             double part = 0.0;
             for (int r = j + 1 + tid; r < n; r += blockDim.x) part += x[r] * x[r];
 #pragma unroll
             for (int off = 16; off; off >>= 1) part += __shfl_down_sync(0xffffffffu, part, off);
             if (lane == 0) red[warp] = part;
             __syncthreads();
+            double xn2 = 0.0;
+            for (int w = 0; w < nwarp; ++w) xn2 += red[w];
+            const double alpha = x[j];
+            double t_, sc, be;
+            if (xn2 == 0.0) { t_ = 0.0; be = alpha; sc = 0.0; }
+            else {
+                be = -copysign(sqrt(alpha * alpha + xn2), alpha);
+                t_ = (be - alpha) / be;
+                sc = 1.0 / (alpha - be);
+            }
+            for (int r = j + 1 + tid; r < n; r += blockDim.x) myv[r] = x[r] * sc;
+            if (tid == 0) { myv[j] = 1.0; mys[1] = t_; mys[2] = be; }
+        }
+        cluster.sync();
+        // ---- the winner (every CTA computes the same one): lane c of warp 0 reads
+        // CTA c's proposal, one DSMEM round trip, then a warp arg-max
+        if (warp == 0) {
+            double ov = -1.0, ot = 0.0;
+            int oi = 0x7fffffff, oc = lane;
+            if (lane < CS) {
+                const double *os = cluster.map_shared_rank(slot, lane) + 4 * par;
+                ov = os[0];
+                ot = os[1];
+                oi = (int)os[3];
+            }
+#pragma unroll
+            for (int off = 16; off; off >>= 1) {
+                const double v2 = __shfl_xor_sync(0xffffffffu, ov, off);
+                const int i2 = __shfl_xor_sync(0xffffffffu, oi, off);
+                const int c2 = __shfl_xor_sync(0xffffffffu, oc, off);
+                const double t2 = __shfl_xor_sync(0xffffffffu, ot, off);
+                if (v2 > ov || (v2 == ov && i2 < oi)) { ov = v2; oi = i2; oc = c2; ot = t2; }
+            }
+            if (lane == 0) { s_win[0] = oi; s_win[1] = oc; s_tau = ot; }
+        }
+        __syncthreads();
+        const int p = s_win[0], wc = s_win[1];
+        const double tj = s_tau;
+        if (wc == crank) {
+            double *x = col + (size_t)(p / CS) * n;
+            double *vrow = M + (int64_t)j * n;
+            for (int r = j + tid; r < n; r += blockDim.x) {
+                const double v = myv[r];
+                vcur[r] = v;
+                vrow[r] = v;
+                if (r > j) x[r] = v;
+            }
             if (tid == 0) {
-                double xn2 = 0.0;
-                for (int w = 0; w < nwarp; ++w) xn2 += red[w];
-                const double alpha = x[j];
-                double t_, sc, be;
-                if (xn2 == 0.0) { t_ = 0.0; be = alpha; sc = 0.0; }
-                else {
-                    be = -copysign(sqrt(alpha * alpha + xn2), alpha);
-                    t_ = (be - alpha) / be;
-                    sc = 1.0 / (alpha - be);
-                }
-                hh[0] = t_; hh[1] = sc; hh[2] = be;
-                tz[j] = t_;
+                x[j] = mys[2];
+                tz[j] = tj;
                 pz[j] = p;
                 usedl[p / CS] = 1;
             }
-            __syncthreads();
-            const double sc = hh[1];
-            double *vrow = M + (int64_t)j * n;
-            for (int r = j + 1 + tid; r < n; r += blockDim.x) {
-                const double v = x[r] * sc;
-                x[r] = v;
-                vbuf[r] = v;
-                vrow[r] = v;
-            }
-            if (tid == 0) { vbuf[j] = 1.0; x[j] = hh[2]; vrow[j] = 1.0; }
-        }
-        cluster.sync();
-        if (owner != crank) {
-            const double *ov = cluster.map_shared_rank(vbuf, owner);
-            for (int r = j + tid; r < n; r += blockDim.x) vbuf[r] = ov[r];
-            if (tid == 0) hh[0] = *cluster.map_shared_rank(hh, owner);
+        } else {
+            const double *ov = cluster.map_shared_rank(vb, wc) + (size_t)par * n;
+            for (int r = j + tid; r < n; r += blockDim.x) vcur[r] = ov[r];
         }
         __syncthreads();
         // ---- apply H_j = I - tau v v^T to the own unused columns; exact trailing norms
-        const double tj = hh[0];
         for (int lc = warp; lc < nloc; lc += nwarp) {
             if (usedl[lc]) continue;
             double *y = col + (size_t)lc * n;
             double sdot = 0.0;
-            for (int r = j + lane; r < n; r += 32) sdot += vbuf[r] * y[r];
+            for (int r = j + lane; r < n; r += 32) sdot += vcur[r] * y[r];
 #pragma unroll
             for (int off = 16; off; off >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, off);
             const double f = tj * sdot;
             double nn = 0.0;
             for (int r = j + lane; r < n; r += 32) {
-                const double v = y[r] - f * vbuf[r];
+                const double v = y[r] - f * vcur[r];
                 y[r] = v;
                 if (r > j) nn += v * v;
             }
@@ -442,7 +461,7 @@ __global__ void __launch_bounds__(FQ_WARPS * 32) form_q_rows_kernel(const double
 
 size_t pqr_cluster_smem(int n, int cs) {
     const int nloc = (n + cs - 1) / cs;
-    return sizeof(double) * ((size_t)nloc * n + n + nloc + 2 + 40 + 4) + sizeof(int) * (2 + nloc + 2);
+    return sizeof(double) * ((size_t)nloc * n + 3 * (size_t)n + nloc + 8 + 32) + sizeof(int) * (nloc + 2);
 }
 
 template <int CS>

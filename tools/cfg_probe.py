@@ -18,7 +18,9 @@ ranks = [b.rank for (l, i), b in Hd.bases.items() if l == L]
 print(f"{name} n={cloud.n} depth={L} build {t1 - t0:.1f}s arena {Hd._arena.numel() * 8 / 1e9:.2f} GB "
       f"dense pairs {len(Hd.structure.dense)} leaf rank mean {np.mean(ranks):.1f} max {max(ranks)} "
       f"max rank all {Hd.max_rank()}", flush=True)
+t_up = time.perf_counter()
 eng = _native.engine_for(Hd, 0)
+print(f"upload {time.perf_counter() - t_up:.2f} s", flush=True)
 eng.set_option("max_batch", mb)
 eng.set_option("time_kernels", int(os.environ.get("TK", "1")))
 eng.set_option("concurrency", int(os.environ.get("C", "2")))
