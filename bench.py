@@ -1,7 +1,7 @@
 """Benchmark: H2-LDL inertia evaluations/s and s per k-th eigenvalue on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config cfg2|cfg1] [--batch S] [--eig]
+                    [--config cfg2|cfg1|cfg3|cfg4|cfg5] [--batch S] [--eig]
 
 Workload (`config.workload`, BASELINE.json configs[1] = "cfg2" by default):
 3D 1/r kernel (A_ii = 0), n = 65,536 uniform points in [0,1]^3 (seed 0,
@@ -139,6 +139,8 @@ class Workload:
     name = ""
     n = 0
     k = 0
+    ks = ()
+    eps_ev = EPS_EV
     interval = (0.0, 0.0)
     H = None
     host_H = None
@@ -147,13 +149,23 @@ class Workload:
     eigs = None        # exact spectrum when known (cfg1 golden)
 
 
-def workload_cfg2(device=True):
-    from paper_2311_08618_b200 import gpu_build
+_CFG_TEXT = {
+    "cfg2": ("1/r (A_ii = 0)", "uniform [0,1]^3 seed 0"),
+    "cfg3": ("-log r (A_ii = 1)", "512x256 jittered lattice in [0,1]^2 seed 0"),
+    "cfg4": ("exp(-r)/r (A_ii = 0)", "uniform on the unit sphere seed 0"),
+    "cfg5": ("-exp(-r/1.42) (A_ii = 0)", "helical nanotube lattice, 1% jitter, seed 0"),
+}
 
+
+def workload_device(name):
+    """BASELINE configs 2-5: H built on the device, Gershgorin interval on the device."""
+    from paper_2311_08618_b200 import configs, gpu_build
+
+    cfg = configs.CONFIGS[name]
     w = Workload()
-    w.name = "cfg2"
+    w.name = name
     t0 = time.perf_counter()
-    w.H, cloud = gpu_build.config_device("cfg2")
+    w.H, cloud = gpu_build.config_device(name)
     import torch
 
     torch.cuda.synchronize()
@@ -162,10 +174,13 @@ def workload_cfg2(device=True):
     w.interval = gpu_build.gershgorin_device(w.H._kernel)
     w.interval_s = time.perf_counter() - t0
     w.n = cloud.n
-    w.k = w.n // 2
-    w.config = {"workload": "cfg2", "n": w.n, "kernel": "1/r (A_ii = 0)",
-                "points": "uniform [0,1]^3 seed 0", "leaf": 256, "eta": 1.0, "eps": 1e-8,
-                "eps_ev": EPS_EV, "k": w.k, "interval": "Gershgorin row sums of A (device)"}
+    w.eps_ev = cfg.eps_ev
+    w.ks = list(cfg.ks)
+    w.k = w.ks[len(w.ks) // 2]
+    kern, pts = _CFG_TEXT[name]
+    w.config = {"workload": name, "n": w.n, "kernel": kern, "points": pts, "leaf": cfg.leaf,
+                "eta": cfg.eta, "eps": cfg.eps, "eps_ev": cfg.eps_ev, "k": w.k,
+                "interval": "Gershgorin row sums of A (device)"}
     return w
 
 
@@ -184,6 +199,8 @@ def workload_cfg1():
     w.eigs = z["eigs"]
     w.n = cloud.n
     w.k = w.n // 2
+    w.ks = [w.k]
+    w.eps_ev = EPS_EV
     w.config = {"workload": "cfg1", "n": w.n, "kernel": "1/r (A_ii = 0)", "leaf": 128,
                 "eta": 1.0, "eps": 1e-8, "eps_ev": EPS_EV, "k": w.k,
                 "interval": "reference Gershgorin interval (tests/golden/cfg1.npz)"}
@@ -191,7 +208,7 @@ def workload_cfg1():
 
 
 def make_workload(name):
-    return workload_cfg2() if name == "cfg2" else workload_cfg1()
+    return workload_cfg1() if name == "cfg1" else workload_device(name)
 
 
 def rounds_needed(interval, eps_ev, q):
@@ -253,7 +270,7 @@ def cpu_baseline(wl, mus, elim_per_eval, seconds):
     fl, dt, nc, full = oracle_sample(host_H, float(mus[0]), seconds, cache)
     rate = fl / dt
     return {"value": rate / elim_per_eval, "unit": UNIT, "cores": _blas_threads(), "kind": "port",
-            "sample": f"first {dt:.1f} s of one cfg2 factorization at mu={float(mus[0]):.6g} "
+            "sample": f"first {dt:.1f} s of one {wl.name} factorization at mu={float(mus[0]):.6g} "
                       f"({nc} leaf clusters eliminated, {fl / 1e12:.2f} of "
                       f"{elim_per_eval / 1e12:.1f} elimination TFLOP; oracle/engine_ref.py on "
                       f"the same H exported to host memory), scaled by the flop fraction",
@@ -282,7 +299,7 @@ def run_ours(args):
     _native.set_default_device(local)
     wl = make_workload(args.config)
     H = wl.H
-    S = args.batch or (7 if wl.name == "cfg2" else 255)
+    S = args.batch or {"cfg1": 255, "cfg2": 7}.get(wl.name, 15)
     eng = _native.engine_for(H, local)
     eng.set_option("max_batch", S)
     eng.set_option("concurrency", 1)
@@ -333,7 +350,7 @@ def run_ours(args):
 
     cache = InertiaCache()
     try:
-        multisection(H, [wl.k], wl.interval, EPS_EV, cache=cache, batch=S * world,
+        multisection(H, [wl.k], wl.interval, wl.eps_ev, cache=cache, batch=S * world,
                      evaluate=evaluate)
     except _Stop:
         pass
@@ -391,9 +408,9 @@ def run_ours(args):
     e2e = n_all / t_e2e if t_e2e > 0 else None
     # ---- eigenvalue: projection from the measured rounds; --eig runs the search
     q = max(1, int(math.floor(math.log2(S * world + 1))))
-    levels, nrounds = rounds_needed(wl.interval, EPS_EV, q)
+    levels, nrounds = rounds_needed(wl.interval, wl.eps_ev, q)
     step_s = t_dev / max(1, len(timed))
-    eig = {"k": wl.k, "eps_ev": EPS_EV, "bisection_levels": levels,
+    eig = {"k": wl.k, "eps_ev": wl.eps_ev, "bisection_levels": levels,
            "multisection_rounds": nrounds, "shifts_per_round": S * world,
            "s_per_eigenvalue_multisection": nrounds * step_s,
            "s_per_eigenvalue_sequential": levels * (sum(single) / 1e3 / max(1, len(single))),
@@ -402,13 +419,13 @@ def run_ours(args):
                    " levels x measured one-shift step (sequential bisection)"}
     if args.eig:
         eng.set_option("time_kernels", 0)
-        ks = [1, wl.k, wl.n] if wl.name == "cfg2" else [wl.k]
+        ks = list(wl.ks)
         ev = sharded if world > 1 else (lambda mus: local_eval(mus))
         state["phase"] = "eig"
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        ests = multisection(H, ks, wl.interval, EPS_EV, cache=InertiaCache(),
+        ests = multisection(H, ks, wl.interval, wl.eps_ev, cache=InertiaCache(),
                             batch=S * world, evaluate=ev)
         t_eig = time.perf_counter() - t0
         eig["measured"] = {"ks": ks, "wall_s": t_eig, "s_per_eigenvalue": t_eig / len(ks),
@@ -429,8 +446,7 @@ def run_ours(args):
         "config": dict(wl.config, shifts_per_step=S * world, shifts_per_rank=S,
                        parallelism=f"shift-sharded multisection x{world} (NCCL all-gather of counts)"
                        if world > 1 else "single GPU",
-                       l2="inputs larger than L2 (H 12.3 GB + ~16 GB per shift of working blocks)"
-                       if wl.name == "cfg2" else "inputs larger than L2"),
+                       l2="inputs larger than L2 (H and the per-shift working blocks are GBs)"),
         "roofline": {"bound": "tensor", "kernel": "schur_gemm_kernel (K6 Schur update, DMMA fp64)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": None,
@@ -517,11 +533,15 @@ def run_reference(args):
         sample = (f"{cores} worker processes x 1 whole factorization per step "
                   f"(oracle/engine_ref.py, OPENBLAS_NUM_THREADS=1)")
         cfg = {"workload": "cfg1", "n": 2048, "leaf": 128, "eps": 1e-8}
+    elif args.config != "cfg2":
+        print(json.dumps({"impl": "reference", "unavailable": "the reference arm samples configs 1 "
+                          "and 2 (per-evaluation flop totals are recorded for those)"}), flush=True)
+        return
     else:
         from paper_2311_08618_b200 import gpu_build
         from oracle import engine_ref
 
-        wl = workload_cfg2()
+        wl = workload_device(args.config)
         # the input H is built on the device (the CPU construction takes ~500 s); the
         # timed path -- the factorization -- is the oracle port on the host
         host_H = gpu_build.to_host(wl.H)
@@ -572,7 +592,7 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg1"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg1", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--batch", type=int, default=0, help="shifts per GPU per step")
     ap.add_argument("--eig", action="store_true", help="run the eigenvalue searches to the end")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
