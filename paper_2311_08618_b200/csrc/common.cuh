@@ -136,11 +136,6 @@ cudaError_t launch_pqr(double *GT, int64_t gstride, int c, int nR, int ldg, doub
                        int *used, double *norms, int64_t vstride, int64_t cstride,
                        const double *tol, int *rank, double *dropped, const int *active,
                        int target, int nshift, cudaStream_t st);
-cudaError_t launch_pchol(const double *M, int64_t mstride, int n, double *S, double *L,
-                         const int *active, int nshift, cudaStream_t st);
-cudaError_t launch_hqr(const double *A, int64_t astride, int n, double *W, double *QT,
-                       double *tau, int64_t tstride, const int *active, int nshift,
-                       cudaStream_t st);
 cudaError_t launch_tail_rank(const double *DT, int64_t dstride, int c, int n, double *part,
                              const double *tol, int *rank, double *dropped, int *r1out,
                              const int *active, int nshift, cudaStream_t st);

@@ -1,22 +1,20 @@
-// Fill recompression rank-reveal (K7): column-pivoted Householder QR with the
-// reference's absolute Frobenius-tail stopping rule.
+// Recompression ordering (K7): column-pivoted Householder QR of the n x n Gram
+// matrix M = G G^T of a cluster's fill rows (engine.cu recompress; the rank is
+// then taken from exact energies in k_rrqr.cu).
 //
-// Reference: gldl.py:67-79 runs scipy.linalg.qr(G, mode="full",
-// pivoting=True) (dgeqp3 + dorgqr) on the full G and then picks
-// rank = first r with sqrt(sum_{i>=r} ||R[i,:]||^2) <= drop_tol.  After r
-// Householder steps that tail is exactly the Frobenius norm of the not yet
-// reduced trailing block, so the factorization can stop as soon as it drops
-// under the tolerance: only t << min(G.shape) steps are performed, and the
-// completion Q[:, t:] is taken from the same reflectors (any orthonormal
-// completion spans the same redundant space; inertia is invariant to the
-// choice).  Column norms are recomputed exactly after every step (no
-// downdating), ties pick the lowest column.
-//
-// Storage: GT = G^T (cols(G) x rows(G), row-major) so each column of G is a
-// contiguous row; one CTA per shift; warps own columns, lanes own rows.
-// Phase A stops on the tolerance; phase B continues every shift to the
-// common rank t = max over shifts (shift-batched structure); form_q builds
-// Tr = [U_r^T ; U_s^T] (rows(G) x rows(G)) from the reflectors.
+// Reference: gldl.py:67-79 runs scipy.linalg.qr(G, mode="full", pivoting=True)
+// on G itself (n_R x c, c up to ~10^5) and keeps the first t directions whose
+// Frobenius tail exceeds drop_tol.  Here the ordering comes from the Gram
+// matrix (n_R x n_R):
+//   * pqr_cluster_kernel: M in the distributed shared memory of a thread-block
+//     cluster, one cluster barrier per column (primary path, n up to ~900);
+//   * form_q_rows_kernel: Q^T from the reflectors, rows in parallel;
+//   * pqr_kernel / form_tr_kernel: single-CTA fallback on M in global memory
+//     (larger n), also usable with the reference's tolerance stop directly on
+//     G^T (target -1) or continued to a common rank (target >= 0).
+// Column norms are recomputed exactly after every step (no downdating), ties
+// pick the lowest column.  Storage: GT = G^T row-major (a column of G is a
+// contiguous row); M is symmetric, so its rows are its columns.
 #include "common.cuh"
 
 #include <cooperative_groups.h>
