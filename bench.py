@@ -439,6 +439,16 @@ def run_ours(args):
         return
     peak = measure_fp64_peak(torch, "cuda")
     achieved = schur_flops / (ms_schur / 1e3) / 1e12 if ms_schur > 0 else None
+    traffic = None
+    try:  # DRAM bytes per Schur launch from the committed ncu --set full capture (config 2)
+        with open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")) as f:
+            tr = json.load(f)
+        if wl.name == "cfg2":
+            traffic = {"dram_bytes_per_launch": tr["dram_bytes_per_launch_mean"],
+                       "algorithmic_bytes_per_launch": tr["algorithmic_bytes_per_launch_mean"],
+                       "source": "profiles/r1_ncu_traffic.json"}
+    except (OSError, KeyError, ValueError):
+        pass
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": len(timed),
         "warmup": W, "ms_per_step": 1e3 * t_dev / max(1, len(timed)), "higher_is_better": True,
@@ -447,9 +457,11 @@ def run_ours(args):
                        parallelism=f"shift-sharded multisection x{world} (NCCL all-gather of counts)"
                        if world > 1 else "single GPU",
                        l2="inputs larger than L2 (H and the per-shift working blocks are GBs)"),
-        "roofline": {"bound": "tensor", "kernel": "schur_gemm_kernel (K6 Schur update, DMMA fp64)",
+        "roofline": {"bound": "tensor", "kernel": "schur_sym_kernel (K6 Schur update, DMMA fp64)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": None,
+                     "frac": (achieved / peak) if achieved else None,
+                     "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
+                     "traffic_detail": traffic,
                      "peak_source": "measured in-run: cuBLAS DGEMM fp64 8192^3 best of 5 "
                                     "(MEASURED_PEAKS.json has no fp64 figure)",
                      "schur_share_of_step": ms_schur / ms if ms else None,

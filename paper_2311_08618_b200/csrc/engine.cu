@@ -135,6 +135,7 @@ public:
     void set_option(const std::string &k, int64_t v) {
         if (k == "max_batch") max_batch_ = (int)std::max<int64_t>(1, v);
         else if (k == "time_kernels") time_kernels_ = (int)v;  // 0 off, 1 every kind, 2 Schur only
+        else if (k == "schur_persist") schur_persist_ = v != 0;
         else throw CudaFail(H2L_EINVAL, "unknown option " + k);
     }
 
@@ -266,7 +267,7 @@ public:
         ranges_ = o.ranges_; boff_ = o.boff_; brank_ = o.brank_; bdim_ = o.bdim_;
         dense_ = o.dense_; lowrank_ = o.lowrank_; deferred_ = o.deferred_; coup_off_ = o.coup_off_;
         arena_ = o.arena_; skel_ = o.skel_; skel_diag_ = o.skel_diag_; skel_off_ = o.skel_off_;
-        max_batch_ = o.max_batch_; time_kernels_ = o.time_kernels_;
+        max_batch_ = o.max_batch_; time_kernels_ = o.time_kernels_; schur_persist_ = o.schur_persist_;
         owns_payload_ = false;
         uploaded_ = o.uploaded_;
     }
@@ -289,6 +290,7 @@ private:
     Staging stage_;
     int max_batch_ = 64;
     int time_kernels_ = 0;
+    bool schur_persist_ = true;
     bool uploaded_ = false;
     cudaEvent_t ev_call_[2];
     std::vector<cudaEvent_t> ev_pool_;
@@ -953,15 +955,22 @@ private:
             // deflation pass: the Gram matrix only orders directions whose energy is above
             // ~1e-16 of the largest; re-order the rest from their own Gram matrix
             {
-                std::vector<int> r1v(s_), a1(s_);
+                std::vector<int> r1v(s_), a1(s_), t1v(s_);
                 CK(cudaMemcpyAsync(r1v.data(), d_r1, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
                 CK(cudaMemcpyAsync(a1.data(), d_active, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
+                CK(cudaMemcpyAsync(t1v.data(), d_rank_, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
                 sync();
-                int r1 = nR;
+                int r1 = nR, t1 = 0;
                 for (int z = 0; z < s_; ++z)
-                    if (a1[z]) r1 = std::min(r1, r1v[z]);
+                    if (a1[z]) {
+                        r1 = std::min(r1, r1v[z]);
+                        t1 = std::max(t1, t1v[z]);
+                    }
                 const int nT = nR - r1;
-                if (nT > 1) {
+                // when the first pass already drops every direction past r1 (t1 <= r1)
+                // re-ordering them cannot change the rank: the tail sums from any
+                // r <= r1 include the whole (rotation-invariant) energy of that subspace
+                if (nT > 1 && t1 > r1) {
                     Blk M2 = alloc(nT, nT, false), Q2T = alloc(nT, nT, false);
                     Blk DT2 = alloc(c, nT, false), QT2 = alloc(nT, nR, false);
                     {
@@ -1249,7 +1258,7 @@ private:
                 {
                     Timed tm(this, 1);
                     launch_schur_sym(Xb.p, Bg.p, Xb.bs, nR, R, nR, d_seg, d_start, ns, d_tbl, s_,
-                                     st_);
+                                     st_, schur_persist_);
                 }
                 CK(cudaGetLastError());
                 dbg_sync("schur-sym");
@@ -1968,6 +1977,46 @@ __global__ void naive_gemm_kernel(const GemmTask *tasks, int ntasks) {
     }
 }
 }  // namespace h2l
+
+// Gram-matrix ordering of the recompression (k_qr.cu): `count` symmetric n x n
+// matrices (host, row-major) -> Q^T (count x n x n), tau, piv; mode 0 the cluster
+// kernel pair, mode 1 the single-CTA fallback pair
+extern "C" int h2l_internal_gram_order(int device, int mode, int n, int count, const double *m,
+                                       double *qt, double *tau, int *piv) {
+    return guarded(nullptr, [&] {
+        CK(cudaSetDevice(device));
+        const int64_t nn = (int64_t)n * n, ts = n;
+        double *dm, *dq, *dt, *dnorm, *dtol, *ddrop;
+        int *dp, *du, *drank;
+        CK(cudaMalloc(&dm, sizeof(double) * nn * count));
+        CK(cudaMalloc(&dq, sizeof(double) * nn * count));
+        CK(cudaMalloc(&dt, sizeof(double) * ts * count));
+        CK(cudaMalloc(&dnorm, sizeof(double) * ts * count));
+        CK(cudaMalloc(&dtol, sizeof(double) * count));
+        CK(cudaMalloc(&ddrop, sizeof(double) * count));
+        CK(cudaMalloc(&dp, sizeof(int) * ts * count));
+        CK(cudaMalloc(&du, sizeof(int) * ts * count));
+        CK(cudaMalloc(&drank, sizeof(int) * count));
+        CK(cudaMemcpy(dm, m, sizeof(double) * nn * count, cudaMemcpyHostToDevice));
+        CK(cudaMemset(dtol, 0, sizeof(double) * count));
+        if (mode == 0) {
+            if (!h2l::pqr_cluster_size(n)) throw h2l::CudaFail(H2L_EINVAL, "n too large for the cluster QR");
+            CK(h2l::launch_pqr_cluster(dm, nn, n, dt, dp, ts, nullptr, count, 0));
+            CK(h2l::launch_form_q_rows(dm, nn, n, dt, ts, dq, nn, nullptr, count, 0));
+        } else {
+            CK(h2l::launch_pqr(dm, nn, n, n, n, dt, dp, du, dnorm, ts, ts, dtol, drank, ddrop, nullptr,
+                               -2, count, 0));
+            CK(h2l::launch_form_tr(dm, nn, n, dt, dp, ts, n, n, dq, nn, nullptr, count, 0));
+        }
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpy(qt, dq, sizeof(double) * nn * count, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(tau, dt, sizeof(double) * ts * count, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(piv, dp, sizeof(int) * ts * count, cudaMemcpyDeviceToHost));
+        for (void *p : {(void *)dm, (void *)dq, (void *)dt, (void *)dnorm, (void *)dtol, (void *)ddrop,
+                        (void *)dp, (void *)du, (void *)drank})
+            cudaFree(p);
+    });
+}
 
 // engine-mode BK of `count` n x n row-major matrices (host), single-CTA (mode 0)
 // or cluster (mode 1) kernel: factor (lower triangle), perm, dinfo, counts, status

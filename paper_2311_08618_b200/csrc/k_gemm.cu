@@ -116,11 +116,37 @@ struct Loader {
 
 // K loop of one BM x BN tile: acc += op(A)[m0:, :] op(B)[:, n0:] (cp.async
 // pipeline, DMMA.8x8x4).  Shared by the grouped GEMM and the Schur kernel.
+// issue (and commit) the first STAGES-1 K chunks of a tile
+template <class Cfg>
+__device__ __forceinline__ void tile_prologue(const double *A, int lda, int tA, int M,
+                                              const double *B, int ldb, int b_trans, int N, int K,
+                                              int m0, int n0) {
+    constexpr int BM = Cfg::BM, BN = Cfg::BN, STAGES = Cfg::STAGES;
+    constexpr int BK = Cfg::BK, SK = Cfg::SK, THREADS = Cfg::THREADS;
+    extern __shared__ __align__(16) double gsm[];
+    const int tid = threadIdx.x;
+    const int nk = (K + BK - 1) / BK;
+    const Loader<BM, THREADS, BK, SK> la(A, lda, tA, M, m0, tid);
+    const Loader<BN, THREADS, BK, SK> lb(B, ldb, b_trans, N, n0, tid);
+    const unsigned sA = (unsigned)__cvta_generic_to_shared(gsm);
+    const unsigned sB = (unsigned)__cvta_generic_to_shared(gsm + STAGES * BM * SK);
+    constexpr unsigned SA_STAGE = BM * SK * sizeof(double), SB_STAGE = BN * SK * sizeof(double);
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < nk) {
+            la.load(sA + s * SA_STAGE, s, K);
+            lb.load(sB + s * SB_STAGE, s, K);
+        }
+        cp_commit();
+    }
+}
+
 template <class Cfg>
 __device__ __forceinline__ void tile_mainloop(const double *A, int lda, int tA, int M,
                                               const double *B, int ldb, int b_trans, int N, int K,
                                               int m0, int n0, int wm, int wn,
-                                              double (&acc)[Cfg::FM][Cfg::FN][2]) {
+                                              double (&acc)[Cfg::FM][Cfg::FN][2],
+                                              bool preissued = false) {
     constexpr int BM = Cfg::BM, BN = Cfg::BN, STAGES = Cfg::STAGES, FM = Cfg::FM, FN = Cfg::FN;
     constexpr int BK = Cfg::BK, SK = Cfg::SK, THREADS = Cfg::THREADS;
     extern __shared__ __align__(16) double gsm[];
@@ -137,13 +163,15 @@ __device__ __forceinline__ void tile_mainloop(const double *A, int lda, int tA, 
     const unsigned sA = (unsigned)__cvta_generic_to_shared(&As[0][0][0]);
     const unsigned sB = (unsigned)__cvta_generic_to_shared(&Bs[0][0][0]);
     constexpr unsigned SA_STAGE = BM * SK * sizeof(double), SB_STAGE = BN * SK * sizeof(double);
+    if (!preissued) {
 #pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-        if (s < nk) {
-            la.load(sA + s * SA_STAGE, s, K);
-            lb.load(sB + s * SB_STAGE, s, K);
+        for (int s = 0; s < STAGES - 1; ++s) {
+            if (s < nk) {
+                la.load(sA + s * SA_STAGE, s, K);
+                lb.load(sB + s * SB_STAGE, s, K);
+            }
+            cp_commit();
         }
-        cp_commit();
     }
     for (int kc = 0; kc < nk; ++kc) {
         cp_wait<STAGES - 2>();
@@ -265,26 +293,79 @@ __device__ __forceinline__ void gemm_body(const GemmTask *tasks, const int *pref
 // per-pair task list padded every segment to a multiple of 64); the epilogue
 // scatters element (r, c), r <= c, to its target block through the
 // segment-pair table (diagonal segments also write the mirrored element).
+// upper-triangular tile index -> (I <= J)
+__device__ __forceinline__ void tri_tile(int t, int &I, int &J) {
+    J = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((J + 1) * (J + 2) / 2 <= t) ++J;
+    while (J * (J + 1) / 2 > t) --J;
+    I = t - J * (J + 1) / 2;
+}
+
+template <class Cfg>
+__device__ __forceinline__ void schur_sym_epilogue(double (&acc)[Cfg::FM][Cfg::FN][2], int m0,
+                                                   int n0, int z, int R, const int *seg_of,
+                                                   const int *seg_start, int nseg,
+                                                   const SchurTarget *tbl);
+
 template <class Cfg>
 __device__ __forceinline__ void schur_sym_body(const double *X, const double *Bg, int64_t sx,
                                                int ld, int R, int K, const int *seg_of,
                                                const int *seg_start, int nseg,
-                                               const SchurTarget *tbl) {
+                                               const SchurTarget *tbl, int ntile, int nshift) {
     constexpr int BM = Cfg::BM, BN = Cfg::BN, FM = Cfg::FM, FN = Cfg::FN;
     static_assert(BM == BN, "square tiles");
-    // upper-triangular tile index -> (I <= J)
-    const int t = blockIdx.x;
-    int J = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-    while ((J + 1) * (J + 2) / 2 <= t) ++J;
-    while (J * (J + 1) / 2 > t) --J;
-    const int I = t - J * (J + 1) / 2;
-    const int m0 = I * BM, n0 = J * BN;
-    const int z = blockIdx.y;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    constexpr int WCOLS = BN / Cfg::WN;
+    const int wm = (warp / WCOLS) * Cfg::WM, wn = (warp % WCOLS) * Cfg::WN;
+    if (ntile == 0) {  // one tile per CTA: (blockIdx.x, blockIdx.y) = (tile, shift)
+        int I, J;
+        tri_tile(blockIdx.x, I, J);
+        const int z = blockIdx.y;
+        double acc[FM][FN][2];
+        tile_mainloop<Cfg>(X + z * sx, ld, 0, R, Bg + z * sx, ld, 0, R, K, I * BM, J * BN, wm, wn,
+                           acc);
+        schur_sym_epilogue<Cfg>(acc, I * BM, J * BN, z, R, seg_of, seg_start, nseg, tbl);
+        return;
+    }
+    // persistent: CTAs stride over (shift, tile); the next tile's first K chunk is
+    // loaded while the current tile's epilogue runs
+    const int total = ntile * nshift;
+    int it = blockIdx.x;
+    if (it >= total) return;
+    {
+        int I, J;
+        tri_tile(it % ntile, I, J);
+        const int z = it / ntile;
+        tile_prologue<Cfg>(X + z * sx, ld, 0, R, Bg + z * sx, ld, 0, R, K, I * BM, J * BN);
+    }
+    for (; it < total; it += gridDim.x) {
+        int I, J;
+        tri_tile(it % ntile, I, J);
+        const int z = it / ntile;
+        double acc[FM][FN][2];
+        tile_mainloop<Cfg>(X + z * sx, ld, 0, R, Bg + z * sx, ld, 0, R, K, I * BM, J * BN, wm, wn,
+                           acc, true);
+        const int nx = it + gridDim.x;
+        if (nx < total) {
+            int I2, J2;
+            tri_tile(nx % ntile, I2, J2);
+            const int z2 = nx / ntile;
+            tile_prologue<Cfg>(X + z2 * sx, ld, 0, R, Bg + z2 * sx, ld, 0, R, K, I2 * BM, J2 * BN);
+        }
+        schur_sym_epilogue<Cfg>(acc, I * BM, J * BN, z, R, seg_of, seg_start, nseg, tbl);
+        __syncthreads();  // the epilogue's shared tables are rebuilt by the next tile
+    }
+}
+
+template <class Cfg>
+__device__ __forceinline__ void schur_sym_epilogue(double (&acc)[Cfg::FM][Cfg::FN][2], int m0,
+                                                   int n0, int z, int R, const int *seg_of,
+                                                   const int *seg_start, int nseg,
+                                                   const SchurTarget *tbl) {
+    constexpr int BM = Cfg::BM, BN = Cfg::BN, FM = Cfg::FM, FN = Cfg::FN;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int WCOLS = BN / Cfg::WN;
     const int wm = (warp / WCOLS) * Cfg::WM, wn = (warp % WCOLS) * Cfg::WN;
-    double acc[FM][FN][2];
-    tile_mainloop<Cfg>(X + z * sx, ld, 0, R, Bg + z * sx, ld, 0, R, K, m0, n0, wm, wn, acc);
     // epilogue: the tile's row / column segments and the few segment-pair targets
     // it touches are resolved once into shared memory; then, like the grouped
     // GEMM, all target loads of a fragment row are issued before its stores
@@ -383,8 +464,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) schur_gemm_kernel(con
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) schur_sym_kernel(
     const double *X, const double *Bg, int64_t sx, int ld, int R, int K, const int *seg_of,
-    const int *seg_start, int nseg, const SchurTarget *tbl) {
-    schur_sym_body<Cfg>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl);
+    const int *seg_start, int nseg, const SchurTarget *tbl, int ntile, int nshift) {
+    schur_sym_body<Cfg>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, ntile, nshift);
 }
 
 // production configuration (chosen with tools/gemm_bench.py)
@@ -408,13 +489,28 @@ int schur_sym_tiles(int R) {
 
 void launch_schur_sym(const double *X, const double *Bg, int64_t sx, int ld, int R, int K,
                       const int *seg_of, const int *seg_start, int nseg, const SchurTarget *tbl,
-                      int nshift, cudaStream_t st) {
+                      int nshift, cudaStream_t st, bool persist) {
     const int tiles = schur_sym_tiles(R);
     if (tiles <= 0 || nshift <= 0 || K <= 0) return;
     smem_optin(schur_sym_kernel<Prod>);
+    static int resident = 0;
+    if (!resident) {
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, schur_sym_kernel<Prod>, Prod::THREADS,
+                                                      Prod::SMEM);
+        resident = std::max(1, sms * std::max(1, per));
+    }
+    const int64_t total = (int64_t)tiles * nshift;
+    if (persist && total > resident) {
+        schur_sym_kernel<Prod><<<resident, Prod::THREADS, Prod::SMEM, st>>>(
+            X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, tiles, nshift);
+        return;
+    }
     dim3 grid(tiles, nshift);
     schur_sym_kernel<Prod><<<grid, Prod::THREADS, Prod::SMEM, st>>>(X, Bg, sx, ld, R, K, seg_of,
-                                                                     seg_start, nseg, tbl);
+                                                                     seg_start, nseg, tbl, 0, nshift);
 }
 
 int gemm_tiles(int M, int N) {

@@ -240,3 +240,41 @@ def test_cluster_bk_bit_identical_to_single_cta(n):
     w = [np.linalg.eigvalsh(A[q]) for q in range(count)]
     assert [int(c[0]) for c in outs[1][3]] == [int(np.sum(v < 0)) for v in w]
     assert (outs[0][2][:, 2::3] == 2.0).any()  # 2x2 pivots were exercised
+
+
+@pytest.mark.parametrize("n", [40, 186, 350, 500])
+def test_gram_ordering_cluster_qr(n):
+    """Recompression ordering (k_qr.cu): the cluster pivoted QR of a Gram matrix
+    returns an orthogonal Q^T with Q^T M P upper triangular, the pivots of a
+    column-pivoted QR (scipy/LAPACK dgeqp3 on the same M), and agrees with the
+    single-CTA fallback kernel."""
+    import ctypes
+
+    import scipy.linalg
+
+    lib = _native.load_library()
+    f = lib.h2l_internal_gram_order
+    f.restype = ctypes.c_int
+    rng = np.random.default_rng(n)
+    count = 2
+    G = rng.standard_normal((count, n, 3 * n)) * np.logspace(0, -6, n)[None, :, None]
+    M = np.ascontiguousarray(G @ G.transpose(0, 2, 1))
+    res = []
+    for mode in (0, 1):
+        qt = np.zeros((count, n, n))
+        tau = np.zeros((count, n))
+        piv = np.zeros((count, n), np.int32)
+        rc = f(0, mode, n, count, M.ctypes.data_as(ctypes.c_void_p), qt.ctypes.data_as(ctypes.c_void_p),
+               tau.ctypes.data_as(ctypes.c_void_p), piv.ctypes.data_as(ctypes.c_void_p))
+        assert rc == 0
+        res.append((qt, piv))
+    for q in range(count):
+        qt, piv = res[0][0][q], res[0][1][q]
+        assert np.abs(qt @ qt.T - np.eye(n)).max() < 1e-12
+        R = qt @ M[q][:, piv]
+        assert np.abs(np.tril(R, -1)).max() <= 1e-10 * np.abs(R).max()
+        _, _, P = scipy.linalg.qr(M[q], pivoting=True)
+        k = min(n, 20)  # leading pivots: well separated norms
+        assert np.array_equal(piv[:k], P[:k])
+        assert np.array_equal(piv, res[1][1][q])
+        assert np.abs(qt - res[1][0][q]).max() < 1e-10
