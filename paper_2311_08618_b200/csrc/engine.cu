@@ -290,7 +290,7 @@ private:
     Staging stage_;
     int max_batch_ = 64;
     int time_kernels_ = 0;
-    bool schur_persist_ = true;
+    bool schur_persist_ = false;
     bool uploaded_ = false;
     cudaEvent_t ev_call_[2];
     std::vector<cudaEvent_t> ev_pool_;
