@@ -108,7 +108,7 @@ struct SchurTarget {
 int schur_sym_tiles(int R);
 void launch_schur_sym(const double *X, const double *Bg, int64_t sx, int ld, int R, int K,
                       const int *seg_of, const int *seg_start, int nseg, const SchurTarget *tbl,
-                      int nshift, cudaStream_t st, bool persist = true);
+                      int nshift, cudaStream_t st, int variant = 0);
 int gemm_tiles(int M, int N);
 void launch_gemm(const GemmTask *dev_tasks, const int *dev_tile_prefix, int ntasks,
                  int total_tiles, int nshift, cudaStream_t st, bool schur = false,

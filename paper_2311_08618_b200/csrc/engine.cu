@@ -135,7 +135,7 @@ public:
     void set_option(const std::string &k, int64_t v) {
         if (k == "max_batch") max_batch_ = (int)std::max<int64_t>(1, v);
         else if (k == "time_kernels") time_kernels_ = (int)v;  // 0 off, 1 every kind, 2 Schur only
-        else if (k == "schur_persist") schur_persist_ = v != 0;
+        else if (k == "schur_variant") schur_variant_ = (int)v;
         else throw CudaFail(H2L_EINVAL, "unknown option " + k);
     }
 
@@ -267,7 +267,7 @@ public:
         ranges_ = o.ranges_; boff_ = o.boff_; brank_ = o.brank_; bdim_ = o.bdim_;
         dense_ = o.dense_; lowrank_ = o.lowrank_; deferred_ = o.deferred_; coup_off_ = o.coup_off_;
         arena_ = o.arena_; skel_ = o.skel_; skel_diag_ = o.skel_diag_; skel_off_ = o.skel_off_;
-        max_batch_ = o.max_batch_; time_kernels_ = o.time_kernels_; schur_persist_ = o.schur_persist_;
+        max_batch_ = o.max_batch_; time_kernels_ = o.time_kernels_; schur_variant_ = o.schur_variant_;
         owns_payload_ = false;
         uploaded_ = o.uploaded_;
     }
@@ -290,7 +290,7 @@ private:
     Staging stage_;
     int max_batch_ = 64;
     int time_kernels_ = 0;
-    bool schur_persist_ = false;
+    int schur_variant_ = 0;
     bool uploaded_ = false;
     cudaEvent_t ev_call_[2];
     std::vector<cudaEvent_t> ev_pool_;
@@ -1258,7 +1258,7 @@ private:
                 {
                     Timed tm(this, 1);
                     launch_schur_sym(Xb.p, Bg.p, Xb.bs, nR, R, nR, d_seg, d_start, ns, d_tbl, s_,
-                                     st_, schur_persist_);
+                                     st_, schur_variant_);
                 }
                 CK(cudaGetLastError());
                 dbg_sync("schur-sym");

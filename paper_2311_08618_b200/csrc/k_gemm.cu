@@ -116,37 +116,11 @@ struct Loader {
 
 // K loop of one BM x BN tile: acc += op(A)[m0:, :] op(B)[:, n0:] (cp.async
 // pipeline, DMMA.8x8x4).  Shared by the grouped GEMM and the Schur kernel.
-// issue (and commit) the first STAGES-1 K chunks of a tile
-template <class Cfg>
-__device__ __forceinline__ void tile_prologue(const double *A, int lda, int tA, int M,
-                                              const double *B, int ldb, int b_trans, int N, int K,
-                                              int m0, int n0) {
-    constexpr int BM = Cfg::BM, BN = Cfg::BN, STAGES = Cfg::STAGES;
-    constexpr int BK = Cfg::BK, SK = Cfg::SK, THREADS = Cfg::THREADS;
-    extern __shared__ __align__(16) double gsm[];
-    const int tid = threadIdx.x;
-    const int nk = (K + BK - 1) / BK;
-    const Loader<BM, THREADS, BK, SK> la(A, lda, tA, M, m0, tid);
-    const Loader<BN, THREADS, BK, SK> lb(B, ldb, b_trans, N, n0, tid);
-    const unsigned sA = (unsigned)__cvta_generic_to_shared(gsm);
-    const unsigned sB = (unsigned)__cvta_generic_to_shared(gsm + STAGES * BM * SK);
-    constexpr unsigned SA_STAGE = BM * SK * sizeof(double), SB_STAGE = BN * SK * sizeof(double);
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-        if (s < nk) {
-            la.load(sA + s * SA_STAGE, s, K);
-            lb.load(sB + s * SB_STAGE, s, K);
-        }
-        cp_commit();
-    }
-}
-
 template <class Cfg>
 __device__ __forceinline__ void tile_mainloop(const double *A, int lda, int tA, int M,
                                               const double *B, int ldb, int b_trans, int N, int K,
                                               int m0, int n0, int wm, int wn,
-                                              double (&acc)[Cfg::FM][Cfg::FN][2],
-                                              bool preissued = false) {
+                                              double (&acc)[Cfg::FM][Cfg::FN][2]) {
     constexpr int BM = Cfg::BM, BN = Cfg::BN, STAGES = Cfg::STAGES, FM = Cfg::FM, FN = Cfg::FN;
     constexpr int BK = Cfg::BK, SK = Cfg::SK, THREADS = Cfg::THREADS;
     extern __shared__ __align__(16) double gsm[];
@@ -163,15 +137,13 @@ __device__ __forceinline__ void tile_mainloop(const double *A, int lda, int tA, 
     const unsigned sA = (unsigned)__cvta_generic_to_shared(&As[0][0][0]);
     const unsigned sB = (unsigned)__cvta_generic_to_shared(&Bs[0][0][0]);
     constexpr unsigned SA_STAGE = BM * SK * sizeof(double), SB_STAGE = BN * SK * sizeof(double);
-    if (!preissued) {
 #pragma unroll
-        for (int s = 0; s < STAGES - 1; ++s) {
-            if (s < nk) {
-                la.load(sA + s * SA_STAGE, s, K);
-                lb.load(sB + s * SB_STAGE, s, K);
-            }
-            cp_commit();
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < nk) {
+            la.load(sA + s * SA_STAGE, s, K);
+            lb.load(sB + s * SB_STAGE, s, K);
         }
+        cp_commit();
     }
     for (int kc = 0; kc < nk; ++kc) {
         cp_wait<STAGES - 2>();
@@ -306,54 +278,51 @@ __device__ __forceinline__ void schur_sym_epilogue(double (&acc)[Cfg::FM][Cfg::F
                                                    int n0, int z, int R, const int *seg_of,
                                                    const int *seg_start, int nseg,
                                                    const SchurTarget *tbl);
-
 template <class Cfg>
+__device__ __forceinline__ void schur_target_prefetch(int m0, int n0, int z, int R,
+                                                      const int *seg_of, const int *seg_start,
+                                                      const SchurTarget *tbl, int nseg);
+
+template <class Cfg, int PF>
 __device__ __forceinline__ void schur_sym_body(const double *X, const double *Bg, int64_t sx,
                                                int ld, int R, int K, const int *seg_of,
                                                const int *seg_start, int nseg,
-                                               const SchurTarget *tbl, int ntile, int nshift) {
+                                               const SchurTarget *tbl) {
     constexpr int BM = Cfg::BM, BN = Cfg::BN, FM = Cfg::FM, FN = Cfg::FN;
     static_assert(BM == BN, "square tiles");
     const int tid = threadIdx.x, warp = tid >> 5;
     constexpr int WCOLS = BN / Cfg::WN;
     const int wm = (warp / WCOLS) * Cfg::WM, wn = (warp % WCOLS) * Cfg::WN;
-    if (ntile == 0) {  // one tile per CTA: (blockIdx.x, blockIdx.y) = (tile, shift)
-        int I, J;
-        tri_tile(blockIdx.x, I, J);
-        const int z = blockIdx.y;
-        double acc[FM][FN][2];
-        tile_mainloop<Cfg>(X + z * sx, ld, 0, R, Bg + z * sx, ld, 0, R, K, I * BM, J * BN, wm, wn,
-                           acc);
-        schur_sym_epilogue<Cfg>(acc, I * BM, J * BN, z, R, seg_of, seg_start, nseg, tbl);
-        return;
-    }
-    // persistent: CTAs stride over (shift, tile); the next tile's first K chunk is
-    // loaded while the current tile's epilogue runs
-    const int total = ntile * nshift;
-    int it = blockIdx.x;
-    if (it >= total) return;
-    {
-        int I, J;
-        tri_tile(it % ntile, I, J);
-        const int z = it / ntile;
-        tile_prologue<Cfg>(X + z * sx, ld, 0, R, Bg + z * sx, ld, 0, R, K, I * BM, J * BN);
-    }
-    for (; it < total; it += gridDim.x) {
-        int I, J;
-        tri_tile(it % ntile, I, J);
-        const int z = it / ntile;
-        double acc[FM][FN][2];
-        tile_mainloop<Cfg>(X + z * sx, ld, 0, R, Bg + z * sx, ld, 0, R, K, I * BM, J * BN, wm, wn,
-                           acc, true);
-        const int nx = it + gridDim.x;
-        if (nx < total) {
-            int I2, J2;
-            tri_tile(nx % ntile, I2, J2);
-            const int z2 = nx / ntile;
-            tile_prologue<Cfg>(X + z2 * sx, ld, 0, R, Bg + z2 * sx, ld, 0, R, K, I2 * BM, J2 * BN);
-        }
-        schur_sym_epilogue<Cfg>(acc, I * BM, J * BN, z, R, seg_of, seg_start, nseg, tbl);
-        __syncthreads();  // the epilogue's shared tables are rebuilt by the next tile
+    int I, J;
+    tri_tile(blockIdx.x, I, J);
+    const int z = blockIdx.y;
+    if (PF) schur_target_prefetch<Cfg>(I * BM, J * BN, z, R, seg_of, seg_start, tbl, nseg);
+    double acc[FM][FN][2];
+    tile_mainloop<Cfg>(X + z * sx, ld, 0, R, Bg + z * sx, ld, 0, R, K, I * BM, J * BN, wm, wn, acc);
+    schur_sym_epilogue<Cfg>(acc, I * BM, J * BN, z, R, seg_of, seg_start, nseg, tbl);
+}
+
+// L2 prefetch of a tile's target rows (variant 1): thread t covers row t / 2,
+// columns (t % 2) * 32 .. +32, one prefetch per 8 columns, each address taken
+// from its own segment pair (always inside the target block)
+template <class Cfg>
+__device__ __forceinline__ void schur_target_prefetch(int m0, int n0, int z, int R,
+                                                      const int *seg_of, const int *seg_start,
+                                                      const SchurTarget *tbl, int nseg) {
+    const int tid = threadIdx.x;
+    if (tid >= 2 * Cfg::BM) return;
+    const int rl = tid >> 1, c0 = (tid & 1) * 32;
+    const int r = m0 + rl;
+    if (r >= R) return;
+    const int a = seg_of[r], ra = r - seg_start[a];
+    for (int c = c0; c < c0 + 32; c += 8) {
+        const int cc = n0 + c;
+        if (cc >= R || cc < r) continue;
+        const int b = seg_of[cc];
+        const SchurTarget e = tbl[(size_t)a * nseg + b];
+        if (!e.base || e.trans) continue;
+        const double *pp = e.base + z * e.bs + (int64_t)ra * e.ldc + (cc - seg_start[b]);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(pp));
     }
 }
 
@@ -461,11 +430,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) schur_gemm_kernel(con
     gemm_body<Cfg>(tasks, prefix, ntasks, tile_task);
 }
 
-template <class Cfg>
+template <class Cfg, int PF>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) schur_sym_kernel(
     const double *X, const double *Bg, int64_t sx, int ld, int R, int K, const int *seg_of,
-    const int *seg_start, int nseg, const SchurTarget *tbl, int ntile, int nshift) {
-    schur_sym_body<Cfg>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, ntile, nshift);
+    const int *seg_start, int nseg, const SchurTarget *tbl) {
+    schur_sym_body<Cfg, PF>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl);
 }
 
 // production configuration (chosen with tools/gemm_bench.py)
@@ -487,30 +456,33 @@ int schur_sym_tiles(int R) {
     return nt * (nt + 1) / 2;
 }
 
+// variants (engine option "schur_variant"; tools/ab_option.py): 0 production,
+// 1 + L2 prefetch of the targets, 2 three-stage pipeline at 3 CTAs/SM,
+// 3 K chunks of 32 at 3 CTAs/SM
+using SymV2 = GemmCfg<64, 64, 32, 32, 3, false, 3>;
+using SymV3 = GemmCfg<64, 64, 32, 32, 2, false, 3, 32>;
+
+template <class Cfg, int PF>
+static void launch_sym(const double *X, const double *Bg, int64_t sx, int ld, int R, int K,
+                       const int *seg_of, const int *seg_start, int nseg, const SchurTarget *tbl,
+                       int tiles, int nshift, cudaStream_t st) {
+    smem_optin(schur_sym_kernel<Cfg, PF>);
+    dim3 grid(tiles, nshift);
+    schur_sym_kernel<Cfg, PF><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(X, Bg, sx, ld, R, K, seg_of,
+                                                                      seg_start, nseg, tbl);
+}
+
 void launch_schur_sym(const double *X, const double *Bg, int64_t sx, int ld, int R, int K,
                       const int *seg_of, const int *seg_start, int nseg, const SchurTarget *tbl,
-                      int nshift, cudaStream_t st, bool persist) {
+                      int nshift, cudaStream_t st, int variant) {
     const int tiles = schur_sym_tiles(R);
     if (tiles <= 0 || nshift <= 0 || K <= 0) return;
-    smem_optin(schur_sym_kernel<Prod>);
-    static int resident = 0;
-    if (!resident) {
-        int dev = 0, sms = 0, per = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, schur_sym_kernel<Prod>, Prod::THREADS,
-                                                      Prod::SMEM);
-        resident = std::max(1, sms * std::max(1, per));
+    switch (variant) {
+        case 1: launch_sym<Prod, 1>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, tiles, nshift, st); break;
+        case 2: launch_sym<SymV2, 0>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, tiles, nshift, st); break;
+        case 3: launch_sym<SymV3, 0>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, tiles, nshift, st); break;
+        default: launch_sym<Prod, 0>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, tiles, nshift, st);
     }
-    const int64_t total = (int64_t)tiles * nshift;
-    if (persist && total > resident) {
-        schur_sym_kernel<Prod><<<resident, Prod::THREADS, Prod::SMEM, st>>>(
-            X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, tiles, nshift);
-        return;
-    }
-    dim3 grid(tiles, nshift);
-    schur_sym_kernel<Prod><<<grid, Prod::THREADS, Prod::SMEM, st>>>(X, Bg, sx, ld, R, K, seg_of,
-                                                                     seg_start, nseg, tbl, 0, nshift);
 }
 
 int gemm_tiles(int M, int N) {
