@@ -327,7 +327,54 @@ private:
         return on;
     }
     std::vector<char> elim_, pend_diag_;
-    std::set<Pair> pend_off_;
+    std::set<Pair> pend_off_;          // pending dense leaf blocks (large levels)
+    // flat pair index of the current level (nc_ <= FLAT_MAX): O(1) block lookups
+    // for the ~R^2/2 segment pairs of every elimination step
+    static constexpr int FLAT_MAX = 2048;
+    int nc_ = 0;
+    std::vector<Blk *> offp_, fillp_;
+    std::vector<char> pendf_;
+    int64_t npend_ = 0, npend_diag_ = 0;
+    bool flat() const { return nc_ <= FLAT_MAX; }
+    size_t pidx(const Pair &k) const { return (size_t)k.first * nc_ + k.second; }
+    Blk *off_get(const Pair &k) {
+        if (flat()) return offp_[pidx(k)];
+        auto it = offd_.find(k);
+        return it == offd_.end() ? nullptr : &it->second;
+    }
+    Blk *fill_get(const Pair &k) {
+        if (flat()) return fillp_[pidx(k)];
+        auto it = fill_.find(k);
+        return it == fill_.end() ? nullptr : &it->second;
+    }
+    Blk *off_put(const Pair &k, const Blk &b) {
+        Blk *p = &(offd_[k] = b);
+        if (flat()) offp_[pidx(k)] = p;
+        return p;
+    }
+    Blk *fill_put(const Pair &k, const Blk &b) {
+        Blk *p = &(fill_[k] = b);
+        if (flat()) fillp_[pidx(k)] = p;
+        return p;
+    }
+    void fill_erase(const Pair &k) {
+        fill_.erase(k);
+        if (flat()) fillp_[pidx(k)] = nullptr;
+    }
+    bool pend_test_clear(const Pair &k) {
+        if (flat()) {
+            char &f = pendf_[pidx(k)];
+            if (!f) return false;
+            f = 0;
+            --npend_;
+            return true;
+        }
+        auto it = pend_off_.find(k);
+        if (it == pend_off_.end()) return false;
+        pend_off_.erase(it);
+        --npend_;
+        return true;
+    }
     std::map<Pair, Blk> offd_, coup_, fill_;
     std::vector<std::set<Pair>> adj_off_, adj_fill_, adj_coup_;
     h2l_stats *st_acc_ = nullptr;
@@ -714,6 +761,13 @@ private:
     }
 
     void reset_adjacency(int nclus) {
+        nc_ = nclus;
+        const size_t nn = flat() ? (size_t)nclus * nclus : 0;
+        offp_.assign(nn, nullptr);
+        fillp_.assign(nn, nullptr);
+        pendf_.assign(nn, 0);
+        pend_off_.clear();
+        npend_ = 0;
         adj_off_.assign(nclus, {});
         adj_fill_.assign(nclus, {});
         adj_coup_.assign(nclus, {});
@@ -746,17 +800,20 @@ private:
         diag_.assign(nl, Blk{});
         reset_adjacency(nl);
         pend_diag_.assign(nl, 0);
-        pend_off_.clear();
+        npend_diag_ = 0;
         for (int i = 0; i < nl; ++i) {
             const int m = lsize(i);
             if (m == 0) continue;
             const int r = std::max(0, brank_[node(L, i)]);
             cl_[i] = Cl{m, m - r, r, r};
             pend_diag_[i] = 1;
+            ++npend_diag_;
         }
         for (auto &pr : dense_) {
-            offd_[pr] = Blk{};
-            pend_off_.insert(pr);
+            off_put(pr, Blk{});
+            if (flat()) pendf_[pidx(pr)] = 1;
+            else pend_off_.insert(pr);
+            ++npend_;
             adj_off_[pr.first].insert(pr);
             adj_off_[pr.second].insert(pr);
         }
@@ -767,6 +824,7 @@ private:
     void ensure_diag(int i, CopyBatch &c) {
         if (i >= (int)pend_diag_.size() || !pend_diag_[i]) return;
         pend_diag_[i] = 0;
+        --npend_diag_;
         const int m = lsize(i);
         diag_[i] = alloc(m, m, false);
         CopyTask t = cp(skel_diag_[i], 0, m, diag_[i].p, diag_[i].bs, m, m, m);
@@ -774,16 +832,14 @@ private:
         add_copy(c, t);
     }
     void ensure_off(const Pair &pr, CopyBatch &c) {
-        auto it = pend_off_.find(pr);
-        if (it == pend_off_.end()) return;
-        pend_off_.erase(it);
+        if (!pend_test_clear(pr)) return;
         Blk b = alloc(lsize(pr.first), lsize(pr.second), false);
         add_copy(c, cp(skel_off_.at(pr), 0, b.cols, b.p, b.bs, b.cols, b.rows, b.cols));
-        offd_[pr] = b;
+        off_put(pr, b);
     }
     // every block the recompression and elimination of i can touch
     void ensure_front(int i) {
-        if (pend_off_.empty() && !std::count(pend_diag_.begin(), pend_diag_.end(), 1)) return;
+        if (npend_ == 0 && npend_diag_ == 0) return;
         CopyBatch c;
         ensure_diag(i, c);
         std::vector<int> partners;
@@ -794,7 +850,7 @@ private:
         std::sort(partners.begin(), partners.end());
         for (size_t x = 0; x < partners.size(); ++x) {
             ensure_diag(partners[x], c);
-            if (!pend_off_.empty())
+            if (npend_)
                 for (size_t y = x + 1; y < partners.size(); ++y)
                     ensure_off({partners[x], partners[y]}, c);
         }
@@ -803,8 +859,7 @@ private:
     void ensure_all() {
         CopyBatch c;
         for (int i = 0; i < (int)pend_diag_.size(); ++i) ensure_diag(i, c);
-        std::vector<Pair> rest(pend_off_.begin(), pend_off_.end());
-        for (auto &pr : rest) ensure_off(pr, c);
+        for (auto &pr : dense_) ensure_off(pr, c);
         flush(c, d_mu_);
     }
 
@@ -830,10 +885,10 @@ private:
             CopyBatch c;
             std::vector<Pair> done;
             for (auto &pr : it->second) {
-                auto f = fill_.find(pr);
-                if (f == fill_.end()) continue;
+                Blk *fp = fill_get(pr);
+                if (!fp) continue;
                 Blk &C = coup_.at(pr);
-                Blk &F = f->second;
+                Blk &F = *fp;
                 const int a = pr.first, b = pr.second;
                 const int ra = cl_[a].nR, rb = cl_[b].nR;
                 if (C.p)
@@ -842,8 +897,8 @@ private:
             }
             flush(c);
             for (auto &pr : done) {
-                release(fill_[pr]);
-                fill_.erase(pr);
+                release(*fill_get(pr));
+                fill_erase(pr);
                 adj_fill_[pr.first].erase(pr);
                 adj_fill_[pr.second].erase(pr);
             }
@@ -896,14 +951,14 @@ private:
         if (nR == 0 || keys.empty()) return;
         std::vector<Pair> ks(keys.begin(), keys.end());
         int c = 0;
-        for (auto &k : ks) c += (k.first == i) ? fill_.at(k).cols : fill_.at(k).rows;
+        for (auto &k : ks) c += (k.first == i) ? fill_get(k)->cols : fill_get(k)->rows;
         if (c > 0) {
             // G^T (c x nR): row q = column q of G
             Blk GT = alloc(c, nR, false);
             CopyBatch cb;
             int q0 = 0;
             for (auto &k : ks) {
-                Blk &F = fill_.at(k);
+                Blk &F = *fill_get(k);
                 if (k.first == i) {  // part = F[:nR, :]  -> GT rows = columns of F
                     add_copy(cb, cp(F.p, F.bs, F.cols, GT.at(q0, 0), GT.bs, nR, F.cols, nR, 1));
                     q0 += F.cols;
@@ -1046,7 +1101,7 @@ private:
         CopyBatch z;
         const int keep = ci.nR;
         for (auto &k : ks) {
-            Blk &F = fill_.at(k);
+            Blk &F = *fill_get(k);
             if (keep == 0) continue;
             if (k.first == i) add_copy(z, zero(F.p, F.bs, F.cols, keep, F.cols));
             else add_copy(z, zero(F.p, F.bs, F.cols, F.rows, keep));
@@ -1068,7 +1123,7 @@ private:
         for (auto *store : {&offd_, &fill_}) {
             auto &adj = (store == &offd_) ? adj_off_[i] : adj_fill_[i];
             for (auto &k : adj) {
-                Blk &B = store->at(k);
+                Blk &B = (store == &offd_) ? *off_get(k) : *fill_get(k);
                 Blk N = alloc(B.rows, B.cols, false);
                 if (k.first == i) row_transform(B, N, Tr.p, Tr.bs, nR, nS, t, g1, c1);
                 else col_transform(B, N, Tr.p, Tr.bs, nR, nS, t, g1, c1);
@@ -1139,10 +1194,10 @@ private:
             const int lo = elim_[j] ? cl_[j].nR : 0;
             Seg g{j, lo, cl_[j].m - lo, R, nullptr, 0, 0, 0, lo};
             if (i < j) {  // offd(i,j)[:nR, :]^T : panel rows = columns of the block
-                Blk &O = offd_.at({i, j});
+                Blk &O = *off_get({i, j});
                 g.src = O.p; g.ss = O.bs; g.lds = O.cols; g.trans = 1;
             } else {      // offd(j,i)[:, :nR]
-                Blk &O = offd_.at({j, i});
+                Blk &O = *off_get({j, i});
                 g.src = O.p; g.ss = O.bs; g.lds = O.cols; g.trans = 0;
             }
             segs.push_back(g);
@@ -1187,28 +1242,23 @@ private:
                 } else if (x == 0) {
                     const int j = b.who;
                     if (i < j) {
-                        Blk &O = offd_.at({i, j});
+                        Blk &O = *off_get({i, j});
                         *C = O.at(nR, b.lo); *sC = O.bs; *ldc = O.cols;
                     } else {
-                        Blk &O = offd_.at({j, i});
+                        Blk &O = *off_get({j, i});
                         *C = O.at(b.lo, nR); *sC = O.bs; *ldc = O.cols; *trans = 1;
                     }
                 } else {
                     const Pair key{a.who, b.who};
-                    Blk *T;
-                    auto o = offd_.find(key);
-                    if (o != offd_.end()) {
-                        T = &o->second;
-                    } else {
-                        auto f = fill_.find(key);
-                        if (f == fill_.end()) {
-                            fill_[key] = alloc(cl_[a.who].m, cl_[b.who].m, true);
+                    Blk *T = off_get(key);
+                    if (!T) {
+                        T = fill_get(key);
+                        if (!T) {
+                            T = fill_put(key, alloc(cl_[a.who].m, cl_[b.who].m, true));
                             adj_fill_[a.who].insert(key);
                             adj_fill_[b.who].insert(key);
                             st_acc_->fill_blocks++;
-                            f = fill_.find(key);
                         }
-                        T = &f->second;
                     }
                     *C = T->at(a.lo, b.lo); *sC = T->bs; *ldc = T->cols;
                 }
@@ -1319,7 +1369,7 @@ private:
             for (auto *store : {&offd_, &fill_}) {
                 auto &adj = (store == &offd_) ? adj_off_[i] : adj_fill_[i];
                 for (auto &k : adj) {
-                    Blk &O = store->at(k);
+                    Blk &O = (store == &offd_) ? *off_get(k) : *fill_get(k);
                     Blk N;
                     if (k.first == i) {
                         N = alloc(nS, O.cols, false);
@@ -1393,13 +1443,8 @@ private:
             *rows = c->second.rows; *cols = c->second.cols;
             return c->second.p != nullptr;
         }
-        const Blk *B = nullptr;
-        auto o = offd_.find(k);
-        if (o != offd_.end()) B = &o->second;
-        else {
-            auto f = fill_.find(k);
-            if (f != fill_.end()) B = &f->second;
-        }
+        const Blk *B = off_get(k);
+        if (!B) B = fill_get(k);
         if (!B || !B->p) return false;
         const int ra = cl_[k.first].nR, rb = cl_[k.second].nR;
         *p = B->at(ra, rb); *bs = B->bs; *ld = B->cols;
@@ -1584,12 +1629,12 @@ private:
         diag_ = ndiag;
         reset_adjacency(np);
         for (auto &kv : noffd) {
-            offd_[kv.first] = kv.second;
+            off_put(kv.first, kv.second);
             adj_off_[kv.first.first].insert(kv.first);
             adj_off_[kv.first.second].insert(kv.first);
         }
         for (auto &kv : nfill) {
-            fill_[kv.first] = kv.second;
+            fill_put(kv.first, kv.second);
             adj_fill_[kv.first.first].insert(kv.first);
             adj_fill_[kv.first.second].insert(kv.first);
         }

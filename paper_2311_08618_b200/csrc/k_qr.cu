@@ -393,24 +393,47 @@ __global__ void __launch_bounds__(PQRC_THREADS) pqr_cluster_kernel(double *Mg, i
             for (int r = j + tid; r < n; r += blockDim.x) vcur[r] = ov[r];
         }
         __syncthreads();
-        // ---- apply H_j = I - tau v v^T to the own unused columns; exact trailing norms
-        for (int lc = warp; lc < nloc; lc += nwarp) {
-            if (usedl[lc]) continue;
-            double *y = col + (size_t)lc * n;
-            double sdot = 0.0;
-            for (int r = j + lane; r < n; r += 32) sdot += vcur[r] * y[r];
+        // ---- apply H_j = I - tau v v^T to the own unused columns; exact trailing norms.
+        // A warp takes up to 4 columns at once: their dot products, reductions and
+        // updates are independent, so the shuffle latencies overlap
+        for (int lc0 = warp; lc0 < nloc; lc0 += 4 * nwarp) {
+            double sd[4] = {0.0, 0.0, 0.0, 0.0};
+            bool on[4];
 #pragma unroll
-            for (int off = 16; off; off >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, off);
-            const double f = tj * sdot;
-            double nn = 0.0;
+            for (int u = 0; u < 4; ++u) {
+                const int lc = lc0 + u * nwarp;
+                on[u] = lc < nloc && !usedl[lc];
+            }
             for (int r = j + lane; r < n; r += 32) {
-                const double v = y[r] - f * vcur[r];
-                y[r] = v;
-                if (r > j) nn += v * v;
+                const double vr = vcur[r];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (on[u]) sd[u] += vr * col[(size_t)(lc0 + u * nwarp) * n + r];
             }
 #pragma unroll
-            for (int off = 16; off; off >>= 1) nn += __shfl_down_sync(0xffffffffu, nn, off);
-            if (lane == 0) nrm[lc] = nn;
+            for (int off = 16; off; off >>= 1)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) sd[u] += __shfl_xor_sync(0xffffffffu, sd[u], off);
+            double nn[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int r = j + lane; r < n; r += 32) {
+                const double vr = vcur[r];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (on[u]) {
+                        double *y = col + (size_t)(lc0 + u * nwarp) * n;
+                        const double v = y[r] - (tj * sd[u]) * vr;
+                        y[r] = v;
+                        if (r > j) nn[u] += v * v;
+                    }
+            }
+#pragma unroll
+            for (int off = 16; off; off >>= 1)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) nn[u] += __shfl_down_sync(0xffffffffu, nn[u], off);
+            if (lane == 0)
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (on[u]) nrm[lc0 + u * nwarp] = nn[u];
         }
         __syncthreads();
     }
