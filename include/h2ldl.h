@@ -129,7 +129,9 @@ int h2l_inertia(h2l_engine *engine, const double *mu, int32_t s, int64_t *counts
  * Tuning knobs (key, value): "max_batch" shifts per device wave (default 64);
  * "concurrency" waves in flight on private streams (default 2); "time_kernels"
  * 0 off, 1 CUDA-event timing of every launch kind (stats.ms_kind), 2 the Schur
- * GEMM launches only (stats.ms_schur; negligible overhead).
+ * GEMM launches only (stats.ms_schur; negligible overhead); "borrow_arena" 1:
+ * a device-resident plan arena is used in place by h2l_upload instead of being
+ * copied (it must then outlive the engine); "schur_variant" kernel variant (0).
  */
 int h2l_set_option(h2l_engine *engine, const char *key, int64_t value);
 

@@ -136,9 +136,15 @@ class DeviceEngine:
 
     def upload(self, H):
         plan, keep = build_plan(H)
+        arena = getattr(H, "_arena", None)
         with self.lock:
+            if arena is not None:
+                # device-built H: the engine reads its arena in place (no 2nd copy in HBM)
+                self.set_option("borrow_arena", 1)
             _check(self.lib.h2l_upload(self.handle, ctypes.byref(plan)), self.handle, "h2l_upload")
-        self._keep = keep  # arrays must outlive the call only; kept for debugging
+        # host plan arrays must outlive the call only; a borrowed device arena must
+        # outlive the engine: keep a reference to it
+        self._keep = (keep, arena)
 
     def inertia(self, mus):
         """(counts[s,3] int64, status[s] int32, stats dict) for absolute shifts mus."""

@@ -109,6 +109,8 @@ int schur_sym_tiles(int R);
 void launch_schur_sym(const double *X, const double *Bg, int64_t sx, int ld, int R, int K,
                       const int *seg_of, const int *seg_start, int nseg, const SchurTarget *tbl,
                       int nshift, cudaStream_t st, int variant = 0);
+void launch_sum_partials(const double *in, int64_t zin, int64_t pstride, int nparts, double *out,
+                         int64_t zout, int64_t count, int nshift, cudaStream_t st);
 int gemm_tiles(int M, int N);
 void launch_gemm(const GemmTask *dev_tasks, const int *dev_tile_prefix, int ntasks,
                  int total_tiles, int nshift, cudaStream_t st, bool schur = false,

@@ -136,6 +136,7 @@ public:
         if (k == "max_batch") max_batch_ = (int)std::max<int64_t>(1, v);
         else if (k == "time_kernels") time_kernels_ = (int)v;  // 0 off, 1 every kind, 2 Schur only
         else if (k == "schur_variant") schur_variant_ = (int)v;
+        else if (k == "borrow_arena") borrow_arena_ = v != 0;
         else throw CudaFail(H2L_EINVAL, "unknown option " + k);
     }
 
@@ -167,12 +168,24 @@ public:
         }
         for (int e = 0; e < pl->n_deferred; ++e)
             deferred_[pl->deferred[3 * e]].push_back({pl->deferred[3 * e + 1], pl->deferred[3 * e + 2]});
-        CK(cudaMalloc(&arena_, sizeof(double) * std::max<int64_t>(1, pl->arena_len)));
-        // host or device arena (unified addressing); stream-ordered on st_ and synced
-        // before any kernel reads it
-        CK(cudaMemcpyAsync(arena_, pl->arena, sizeof(double) * pl->arena_len, cudaMemcpyDefault,
-                           st_));
-        CK(cudaStreamSynchronize(st_));
+        cudaPointerAttributes pa{};
+        const bool on_device = cudaPointerGetAttributes(&pa, pl->arena) == cudaSuccess &&
+                               pa.type == cudaMemoryTypeDevice && pa.device == dev_;
+        cudaGetLastError();
+        if (borrow_arena_ && on_device) {
+            // "borrow_arena": the caller's device arena is used in place and must
+            // outlive the engine (the Python layer keeps the device-built H alive)
+            arena_ = const_cast<double *>(pl->arena);
+            owns_arena_ = false;
+        } else {
+            CK(cudaMalloc(&arena_, sizeof(double) * std::max<int64_t>(1, pl->arena_len)));
+            owns_arena_ = true;
+            // host or device arena (unified addressing); stream-ordered on st_ and
+            // synced before any kernel reads it
+            CK(cudaMemcpyAsync(arena_, pl->arena, sizeof(double) * pl->arena_len, cudaMemcpyDefault,
+                               st_));
+            CK(cudaStreamSynchronize(st_));
+        }
         const int L = depth_;
         const int nleaf = 1 << L;
         // ---- skeleton prologue (K1): S = Q^T A Q, shift independent (compress.py:99-127)
@@ -283,7 +296,7 @@ public:
     std::string err;
 
 private:
-    bool owns_payload_ = true;
+    bool owns_payload_ = true, owns_arena_ = true, borrow_arena_ = false;
     cudaMemPool_t pool_ = nullptr;
     int dev_;
     cudaStream_t st_ = nullptr;
@@ -395,7 +408,7 @@ private:
 
     void free_payload() {
         if (owns_payload_) {
-            if (arena_) cudaFree(arena_);
+            if (arena_ && owns_arena_) cudaFree(arena_);
             if (skel_) cudaFree(skel_);
         }
         arena_ = skel_ = nullptr;
@@ -944,6 +957,40 @@ private:
         }
     }
 
+    // M (n x n) = A^T A for A = c x n (row stride ld, shift stride sA).  The
+    // contraction runs over c (up to ~10^5) with only (n/64)^2 output tiles, so it
+    // is split over K into partial products (one grouped launch) summed in a fixed
+    // order by a second kernel: enough CTAs to fill the SMs
+    void gram(const double *A, int64_t sA, int ld, int n, int c, Blk &M) {
+        const int tiles = gemm_tiles(n, n);
+        int parts = std::max(1, std::min((c + 511) / 512, (2 * 148 * 4 + tiles - 1) / std::max(1, tiles)));
+        if (parts <= 1) {
+            GemmBatch g;
+            add_gemm(g, gm(A, sA, ld, 1, A, sA, ld, 0, M.p, M.bs, n, n, n, c, 1.0, 0.0), s_);
+            flush(g, s_, 6);
+            return;
+        }
+        const int chunk = (c + parts - 1) / parts;
+        parts = (c + chunk - 1) / chunk;
+        const int64_t ps = pad4((int64_t)n * n);
+        double *P;
+        CK(cudaMallocFromPoolAsync((void **)&P, sizeof(double) * ps * parts * s_, pool_, st_));
+        GemmBatch g;
+        for (int q = 0; q < parts; ++q) {
+            const int k0 = q * chunk, kc = std::min(chunk, c - k0);
+            add_gemm(g, gm(A + (int64_t)k0 * ld, sA, ld, 1, A + (int64_t)k0 * ld, sA, ld, 0,
+                           P + q * ps, ps * parts, n, n, n, kc, 1.0, 0.0), s_);
+        }
+        flush(g, s_, 6);
+        {
+            Timed tm(this, 6);
+            launch_sum_partials(P, ps * parts, ps, parts, M.p, M.bs, (int64_t)n * n, s_, st_);
+        }
+        CK(cudaGetLastError());
+        st_acc_->launches++;
+        CK(cudaFreeAsync(P, st_));
+    }
+
     void recompress(int i) {
         Cl &ci = cl_[i];
         const int nR = ci.nR;
@@ -984,12 +1031,7 @@ private:
             CK(cudaMallocFromPoolAsync((void **)&part, sizeof(double) * pn * s_, pool_, st_));
             CK(cudaMallocFromPoolAsync((void **)&d_active, sizeof(int) * s_, pool_, st_));
             activity_from_status(d_active);
-            {
-                GemmBatch g;  // M = G G^T = GT^T GT
-                add_gemm(g, gm(GT.p, GT.bs, nR, 1, GT.p, GT.bs, nR, 0, M.p, M.bs, nR, nR, nR, c,
-                               1.0, 0.0), s_);
-                flush(g, s_, 6);
-            }
+            gram(GT.p, GT.bs, nR, nR, c, M);  // M = G G^T = GT^T GT
             {
                 Timed tm(this, 6);
                 gram_order(M, nR, QT, tau, piv, used, norms, ts, d_active);
@@ -1028,12 +1070,7 @@ private:
                 if (nT > 1 && t1 > r1) {
                     Blk M2 = alloc(nT, nT, false), Q2T = alloc(nT, nT, false);
                     Blk DT2 = alloc(c, nT, false), QT2 = alloc(nT, nR, false);
-                    {
-                        GemmBatch g;  // M2 = D_tail D_tail^T (columns r1.. of DT)
-                        add_gemm(g, gm(DT.p + r1, DT.bs, nR, 1, DT.p + r1, DT.bs, nR, 0, M2.p,
-                                       M2.bs, nT, nT, nT, c, 1.0, 0.0), s_);
-                        flush(g, s_, 6);
-                    }
+                    gram(DT.p + r1, DT.bs, nR, nT, c, M2);  // M2 = D_tail D_tail^T
                     {
                         Timed tm(this, 6);
                         gram_order(M2, nT, Q2T, tau, piv, used, norms, ts, d_active);

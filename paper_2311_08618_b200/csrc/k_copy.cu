@@ -81,3 +81,31 @@ int copy_tiles(int rows, int cols) {
 }
 
 }  // namespace h2l
+
+namespace h2l {
+namespace {
+// out[z][e] = sum_s in[z][s * pstride + e], e < count (split-K partial sums, fixed order)
+__global__ void __launch_bounds__(256) sum_partials_kernel(const double *in, int64_t zin,
+                                                           int64_t pstride, int nparts,
+                                                           double *out, int64_t zout,
+                                                           int64_t count) {
+    const int z = blockIdx.y;
+    const double *src = in + z * zin;
+    double *dst = out + z * zout;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int s = 0; s < nparts; ++s) acc += src[s * pstride + e];
+        dst[e] = acc;
+    }
+}
+}  // namespace
+
+void launch_sum_partials(const double *in, int64_t zin, int64_t pstride, int nparts, double *out,
+                         int64_t zout, int64_t count, int nshift, cudaStream_t st) {
+    if (count <= 0 || nshift <= 0) return;
+    const int blocks = (int)std::min<int64_t>(1024, (count + 255) / 256);
+    sum_partials_kernel<<<dim3(blocks, nshift), 256, 0, st>>>(in, zin, pstride, nparts, out, zout,
+                                                               count);
+}
+}  // namespace h2l

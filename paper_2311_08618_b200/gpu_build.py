@@ -290,6 +290,10 @@ def construct_device(kernel, tree, structure, eps, device="cuda", verbose=False)
     H._arena_offsets = offsets
     scale = max((float(b.abs().max()) for b in leaf_diag.values() if b.numel()), default=0.0)
     H._scale0 = scale
+    # hand the construction's temporaries back to the device: the engine allocates
+    # from its own stream-ordered pools, not from torch's cache
+    del bases, expanded
+    t.cuda.empty_cache()
     return H
 
 
