@@ -299,10 +299,15 @@ def run_ours(args):
     _native.set_default_device(local)
     wl = make_workload(args.config)
     H = wl.H
-    S = args.batch or {"cfg1": 255, "cfg2": 7}.get(wl.name, 15)
+    S = args.batch or {"cfg1": 255, "cfg2": 7, "cfg4": 2}.get(wl.name, 15)
     eng = _native.engine_for(H, local)
     eng.set_option("max_batch", S)
     eng.set_option("concurrency", 1)
+    if wl.name == "cfg4":
+        # the unit-sphere front does not fit one B200 in the reference's ascending
+        # order; low-degree-first keeps a shift at ~45 GB (counts are order-free)
+        eng.set_option("elim_order", 1)
+        wl.config["elimination_order"] = "low near-field degree first (ascending needs > 180 GB)"
     # Schur launches timed by CUDA events inside the timed region (the roofline);
     # the per-kind breakdown needs events on every launch and runs after it
     eng.set_option("time_kernels", 2)
@@ -488,7 +493,11 @@ def run_ours(args):
         want = np.searchsorted(wl.eigs, timed_mus[0])
         got = [c.neg for c in inertia_batch(H, timed_mus[0])]
         line["parity_spot_check"] = bool(np.array_equal(np.asarray(got), want))
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and wl.name == "cfg4":
+        line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
+                                "sample": "not runnable: the reference's ascending-order fill for "
+                                          "config 4 is ~200 GB (SURVEY §8d), above the host's RAM"}
+    elif world == 1 and not args.no_cpu_baseline:
         mus = timed_mus[0] if timed_mus else [0.0]
         line["cpu_baseline"] = cpu_baseline(wl, mus, elim / max(1, n_local), args.cpu_seconds)
     print(json.dumps(line), flush=True)

@@ -137,6 +137,7 @@ public:
         else if (k == "time_kernels") time_kernels_ = (int)v;  // 0 off, 1 every kind, 2 Schur only
         else if (k == "schur_variant") schur_variant_ = (int)v;
         else if (k == "borrow_arena") borrow_arena_ = v != 0;
+        else if (k == "elim_order") elim_order_ = (int)v;
         else throw CudaFail(H2L_EINVAL, "unknown option " + k);
     }
 
@@ -280,7 +281,7 @@ public:
         ranges_ = o.ranges_; boff_ = o.boff_; brank_ = o.brank_; bdim_ = o.bdim_;
         dense_ = o.dense_; lowrank_ = o.lowrank_; deferred_ = o.deferred_; coup_off_ = o.coup_off_;
         arena_ = o.arena_; skel_ = o.skel_; skel_diag_ = o.skel_diag_; skel_off_ = o.skel_off_;
-        max_batch_ = o.max_batch_; time_kernels_ = o.time_kernels_; schur_variant_ = o.schur_variant_;
+        max_batch_ = o.max_batch_; time_kernels_ = o.time_kernels_; schur_variant_ = o.schur_variant_; elim_order_ = o.elim_order_;
         owns_payload_ = false;
         uploaded_ = o.uploaded_;
     }
@@ -303,7 +304,7 @@ private:
     Staging stage_;
     int max_batch_ = 64;
     int time_kernels_ = 0;
-    int schur_variant_ = 0;
+    int schur_variant_ = 0, elim_order_ = 0;
     bool uploaded_ = false;
     cudaEvent_t ev_call_[2];
     std::vector<cudaEvent_t> ev_pool_;
@@ -879,7 +880,17 @@ private:
     void process_level(int level) {
         const int nc = 1 << level;
         const bool leaf = level == depth_;
-        for (int i = 0; i < nc; ++i) {
+        // elimination order: ascending (the reference, gldl.py:263) or, with the
+        // "elim_order" option, low near-field degree first (smaller fronts: the
+        // config-4 sphere does not fit one B200 in ascending order); the inertia
+        // is order-independent, the fill pattern and ranks are not
+        std::vector<int> order(nc);
+        for (int i = 0; i < nc; ++i) order[i] = i;
+        if (elim_order_ == 1)
+            std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+                return adj_off_[a].size() + adj_fill_[a].size() < adj_off_[b].size() + adj_fill_[b].size();
+            });
+        for (int i : order) {
             if (cl_[i].m == 0) continue;
             if (leaf) ensure_front(i);
             const auto h0 = std::chrono::steady_clock::now();

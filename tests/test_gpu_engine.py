@@ -278,3 +278,20 @@ def test_gram_ordering_cluster_qr(n):
         assert np.array_equal(piv[:k], P[:k])
         assert np.array_equal(piv, res[1][1][q])
         assert np.abs(qt - res[1][0][q]).max() < 1e-10
+
+
+@pytest.mark.parametrize("name", instance_names()[:8])
+def test_low_degree_first_order_keeps_counts(name):
+    """The optional low-degree-first elimination order (engine option elim_order=1,
+    for fronts that do not fit in ascending order) changes fills and ranks but
+    not the inertia: counts equal the reference's on every golden shift."""
+    H = h2matrix.load_payload(f"tests/golden/h_{name}.npz")
+    z = golden(f"counts_{name}.npz")
+    eng = _native.engine_for(H)
+    try:
+        eng.set_option("elim_order", 1)
+        counts, status, _ = eng.inertia(np.asarray(z["mus"], dtype=np.float64))
+    finally:
+        eng.set_option("elim_order", 0)
+    assert not status.any()
+    assert np.array_equal(counts, z["counts"])
