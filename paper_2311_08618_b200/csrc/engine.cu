@@ -1278,6 +1278,7 @@ private:
                             0.0), s_);
             flush(g0, s_);
             Blk Xb = alloc(R, nR, false);
+            CopyBatch fz;  // zeroing of the fill blocks this step creates
             // target block of a segment pair (x <= y); creates fill blocks (gldl.py:398-409)
             auto target = [&](size_t x, size_t y, double **C, int64_t *sC, int *ldc, int *trans) {
                 const Seg &a = segs[x], &b = segs[y];
@@ -1302,7 +1303,10 @@ private:
                     if (!T) {
                         T = fill_get(key);
                         if (!T) {
-                            T = fill_put(key, alloc(cl_[a.who].m, cl_[b.who].m, true));
+                            // zeroed in one batched launch before the update (fz)
+                            Blk nb = alloc(cl_[a.who].m, cl_[b.who].m, false);
+                            if (nb.p) add_copy(fz, zero(nb.p, nb.bs, nb.cols, nb.rows, nb.cols));
+                            T = fill_put(key, nb);
                             adj_fill_[a.who].insert(key);
                             adj_fill_[b.who].insert(key);
                             st_acc_->fill_blocks++;
@@ -1349,6 +1353,7 @@ private:
                         SchurTarget &e = schur_tbl_[(size_t)x * ns + y];
                         target(x, y, &e.base, &e.bs, &e.ldc, &e.trans);
                     }
+                flush(fz);
                 const int *d_seg = (const int *)stage(seg_of_.data(), sizeof(int) * R);
                 const int *d_start = (const int *)stage(seg_start_.data(), sizeof(int) * ns);
                 const SchurTarget *d_tbl = (const SchurTarget *)stage(
@@ -1391,6 +1396,7 @@ private:
                     add_gemm(g, gm(Xb.at(ra.row, 0), Xb.bs, nR, 0, B, cb.ss, ldb, tB, C, sC, ldc,
                                    ra.len, cb.len, nR, -1.0, 1.0), s_);
                 }
+            flush(fz);
             flush(g, s_, 1);
             }
             flops += sch;
