@@ -144,11 +144,13 @@ cudaError_t launch_tail_rank(const double *DT, int64_t dstride, int c, int n, do
 int64_t tail_rank_part_doubles(int c, int n);
 // cluster-parallel full pivoted QR of an n x n Gram matrix (reflectors to rows of M)
 int pqr_cluster_size(int n);
+// kmax / kref <= 0: all n pivots / reflectors
 cudaError_t launch_pqr_cluster(double *M, int64_t mstride, int n, double *tau, int *piv,
-                               int64_t vstride, const int *active, int nshift, cudaStream_t st);
+                               int64_t vstride, const int *active, int nshift, cudaStream_t st,
+                               int kmax = 0);
 cudaError_t launch_form_q_rows(const double *V, int64_t vstride, int n, const double *tau,
                                int64_t tstride, double *QT, int64_t qstride, const int *active,
-                               int nshift, cudaStream_t st);
+                               int nshift, cudaStream_t st, int kref = 0);
 cudaError_t launch_form_tr(const double *GT, int64_t gstride, int ldg, const double *tau,
                            const int *piv, int64_t vstride, int nR, int t, double *Tr,
                            int64_t tstride, const int *active, int nshift, cudaStream_t st);

@@ -138,6 +138,7 @@ public:
         else if (k == "schur_variant") schur_variant_ = (int)v;
         else if (k == "borrow_arena") borrow_arena_ = v != 0;
         else if (k == "elim_order") elim_order_ = (int)v;
+        else if (k == "qr_budget") qr_budget_ = v != 0;
         else throw CudaFail(H2L_EINVAL, "unknown option " + k);
     }
 
@@ -281,7 +282,7 @@ public:
         ranges_ = o.ranges_; boff_ = o.boff_; brank_ = o.brank_; bdim_ = o.bdim_;
         dense_ = o.dense_; lowrank_ = o.lowrank_; deferred_ = o.deferred_; coup_off_ = o.coup_off_;
         arena_ = o.arena_; skel_ = o.skel_; skel_diag_ = o.skel_diag_; skel_off_ = o.skel_off_;
-        max_batch_ = o.max_batch_; time_kernels_ = o.time_kernels_; schur_variant_ = o.schur_variant_; elim_order_ = o.elim_order_;
+        max_batch_ = o.max_batch_; time_kernels_ = o.time_kernels_; schur_variant_ = o.schur_variant_; elim_order_ = o.elim_order_; qr_budget_ = o.qr_budget_;
         owns_payload_ = false;
         uploaded_ = o.uploaded_;
     }
@@ -305,6 +306,8 @@ private:
     int max_batch_ = 64;
     int time_kernels_ = 0;
     int schur_variant_ = 0, elim_order_ = 0;
+    int t_level_max_ = -1;  // largest recompression rank of the current level (-1: none yet)
+    bool qr_budget_ = true;
     bool uploaded_ = false;
     cudaEvent_t ev_call_[2];
     std::vector<cudaEvent_t> ev_pool_;
@@ -880,6 +883,7 @@ private:
     void process_level(int level) {
         const int nc = 1 << level;
         const bool leaf = level == depth_;
+        t_level_max_ = -1;
         // elimination order: ascending (the reference, gldl.py:263) or, with the
         // "elim_order" option, low near-field degree first (smaller fronts: the
         // config-4 sphere does not fit one B200 in ascending order); the inertia
@@ -955,10 +959,10 @@ private:
     // the cluster kernel keeps M in distributed shared memory; beyond its capacity
     // the single-CTA kernel pair runs on M in global memory
     void gram_order(Blk &M, int n, Blk &QT, double *tau, int *piv, int *used, double *norms,
-                    int64_t ts, const int *d_active) {
+                    int64_t ts, const int *d_active, int kmax) {
         if (pqr_cluster_size(n)) {
-            CK(launch_pqr_cluster(M.p, M.bs, n, tau, piv, ts, d_active, s_, st_));
-            CK(launch_form_q_rows(M.p, M.bs, n, tau, ts, QT.p, QT.bs, d_active, s_, st_));
+            CK(launch_pqr_cluster(M.p, M.bs, n, tau, piv, ts, d_active, s_, st_, kmax));
+            CK(launch_form_q_rows(M.p, M.bs, n, tau, ts, QT.p, QT.bs, d_active, s_, st_, kmax));
         } else {
             // M is symmetric: its row-major storage is also its "columns as rows" layout
             CK(launch_pqr(M.p, M.bs, n, n, n, tau, piv, used, norms, ts, ts, d_tol_, d_rank_,
@@ -1042,85 +1046,99 @@ private:
             CK(cudaMallocFromPoolAsync((void **)&part, sizeof(double) * pn * s_, pool_, st_));
             CK(cudaMallocFromPoolAsync((void **)&d_active, sizeof(int) * s_, pool_, st_));
             activity_from_status(d_active);
-            gram(GT.p, GT.bs, nR, nR, c, M);  // M = G G^T = GT^T GT
-            {
-                Timed tm(this, 6);
-                gram_order(M, nR, QT, tau, piv, used, norms, ts, d_active);
-            }
-            {
-                GemmBatch g;  // D^T = GT Q  (Q[k][n] = QT[n][k])
-                add_gemm(g, gm(GT.p, GT.bs, nR, 0, QT.p, QT.bs, nR, 1, DT.p, DT.bs, nR, c, nR, nR,
-                               1.0, 0.0), s_);
-                flush(g, s_, 6);
-            }
-            int *d_r1;
-            CK(cudaMallocFromPoolAsync((void **)&d_r1, sizeof(int) * s_, pool_, st_));
-            {
-                Timed tm(this, 6);
-                CK(launch_tail_rank(DT.p, DT.bs, c, nR, part, d_tol_, d_rank_, d_dropped_, d_r1,
-                                    d_active, s_, st_));
-            }
-            // deflation pass: the Gram matrix only orders directions whose energy is above
-            // ~1e-16 of the largest; re-order the rest from their own Gram matrix
-            {
-                std::vector<int> r1v(s_), a1(s_), t1v(s_);
-                CK(cudaMemcpyAsync(r1v.data(), d_r1, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
-                CK(cudaMemcpyAsync(a1.data(), d_active, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
-                CK(cudaMemcpyAsync(t1v.data(), d_rank_, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
-                sync();
-                int r1 = nR, t1 = 0;
-                for (int z = 0; z < s_; ++z)
-                    if (a1[z]) {
-                        r1 = std::min(r1, r1v[z]);
-                        t1 = std::max(t1, t1v[z]);
-                    }
-                const int nT = nR - r1;
-                // when the first pass already drops every direction past r1 (t1 <= r1)
-                // re-ordering them cannot change the rank: the tail sums from any
-                // r <= r1 include the whole (rotation-invariant) energy of that subspace
-                if (nT > 1 && t1 > r1) {
-                    Blk M2 = alloc(nT, nT, false), Q2T = alloc(nT, nT, false);
-                    Blk DT2 = alloc(c, nT, false), QT2 = alloc(nT, nR, false);
-                    gram(DT.p + r1, DT.bs, nR, nT, c, M2);  // M2 = D_tail D_tail^T
-                    {
-                        Timed tm(this, 6);
-                        gram_order(M2, nT, Q2T, tau, piv, used, norms, ts, d_active);
-                    }
-                    {
-                        GemmBatch g;  // DT2 = D_tail^T Q2 ; QT2 = Q2^T QT[r1:, :]
-                        add_gemm(g, gm(DT.p + r1, DT.bs, nR, 0, Q2T.p, Q2T.bs, nT, 1, DT2.p, DT2.bs,
-                                       nT, c, nT, nT, 1.0, 0.0), s_);
-                        add_gemm(g, gm(Q2T.p, Q2T.bs, nT, 0, QT.at(r1, 0), QT.bs, nR, 0, QT2.p,
-                                       QT2.bs, nR, nT, nR, nT, 1.0, 0.0), s_);
-                        flush(g, s_, 6);
-                    }
-                    CopyBatch cc;
-                    add_copy(cc, cp(DT2.p, DT2.bs, nT, DT.p + r1, DT.bs, nR, c, nT));
-                    add_copy(cc, cp(QT2.p, QT2.bs, nR, QT.at(r1, 0), QT.bs, nR, nT, nR));
-                    flush(cc);
-                    {
-                        Timed tm(this, 6);
-                        CK(launch_tail_rank(DT.p, DT.bs, c, nR, part, d_tol_, d_rank_, d_dropped_,
-                                            nullptr, d_active, s_, st_));
-                    }
-                    for (Blk *b : {&M2, &Q2T, &DT2, &QT2}) release(*b);
-                    st_acc_->launches += 8;
-                }
-            }
-            CK(cudaFreeAsync(d_r1, st_));
-            st_acc_->launches += 5;
-            std::vector<int> rk(s_), act(s_);
-            std::vector<double> dr(s_);
-            CK(cudaMemcpyAsync(rk.data(), d_rank_, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
-            CK(cudaMemcpyAsync(act.data(), d_active, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
-            CK(cudaMemcpyAsync(dr.data(), d_dropped_, sizeof(double) * s_, cudaMemcpyDeviceToHost, st_));
-            sync();
+            // the ordering is budgeted: kmax pivots (1.5x the largest rank this level
+            // has needed + 32, all of them for the level's first cluster); if the rank
+            // comes within 8 of the budget the ordering is redone with every pivot
+            int kmax = (t_level_max_ < 0 || !qr_budget_)
+                           ? nR : std::min(nR, t_level_max_ + std::max(32, t_level_max_ / 2));
             int t = 0;
-            for (int z = 0; z < s_; ++z)
-                if (act[z]) {
-                    t = std::max(t, rk[z]);
-                    st_acc_->dropped_fro += dr[z];
+            double dropped = 0.0;
+            while (true) {
+                gram(GT.p, GT.bs, nR, nR, c, M);  // M = G G^T = GT^T GT
+                {
+                    Timed tm(this, 6);
+                    gram_order(M, nR, QT, tau, piv, used, norms, ts, d_active, kmax);
                 }
+                {
+                    GemmBatch g;  // D^T = GT Q  (Q[k][n] = QT[n][k])
+                    add_gemm(g, gm(GT.p, GT.bs, nR, 0, QT.p, QT.bs, nR, 1, DT.p, DT.bs, nR, c, nR, nR,
+                                   1.0, 0.0), s_);
+                    flush(g, s_, 6);
+                }
+                int *d_r1;
+                CK(cudaMallocFromPoolAsync((void **)&d_r1, sizeof(int) * s_, pool_, st_));
+                {
+                    Timed tm(this, 6);
+                    CK(launch_tail_rank(DT.p, DT.bs, c, nR, part, d_tol_, d_rank_, d_dropped_, d_r1,
+                                        d_active, s_, st_));
+                }
+                // deflation pass: the Gram matrix only orders directions whose energy is above
+                // ~1e-16 of the largest; re-order the rest from their own Gram matrix
+                {
+                    std::vector<int> r1v(s_), a1(s_), t1v(s_);
+                    CK(cudaMemcpyAsync(r1v.data(), d_r1, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
+                    CK(cudaMemcpyAsync(a1.data(), d_active, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
+                    CK(cudaMemcpyAsync(t1v.data(), d_rank_, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
+                    sync();
+                    int r1 = nR, t1 = 0;
+                    for (int z = 0; z < s_; ++z)
+                        if (a1[z]) {
+                            r1 = std::min(r1, r1v[z]);
+                            t1 = std::max(t1, t1v[z]);
+                        }
+                    const int nT = nR - r1;
+                    // when the first pass already drops every direction past r1 (t1 <= r1)
+                    // re-ordering them cannot change the rank: the tail sums from any
+                    // r <= r1 include the whole (rotation-invariant) energy of that subspace
+                    if (nT > 1 && t1 > r1) {
+                        Blk M2 = alloc(nT, nT, false), Q2T = alloc(nT, nT, false);
+                        Blk DT2 = alloc(c, nT, false), QT2 = alloc(nT, nR, false);
+                        gram(DT.p + r1, DT.bs, nR, nT, c, M2);  // M2 = D_tail D_tail^T
+                        {
+                            Timed tm(this, 6);
+                            gram_order(M2, nT, Q2T, tau, piv, used, norms, ts, d_active, std::min(nT, kmax));
+                        }
+                        {
+                            GemmBatch g;  // DT2 = D_tail^T Q2 ; QT2 = Q2^T QT[r1:, :]
+                            add_gemm(g, gm(DT.p + r1, DT.bs, nR, 0, Q2T.p, Q2T.bs, nT, 1, DT2.p, DT2.bs,
+                                           nT, c, nT, nT, 1.0, 0.0), s_);
+                            add_gemm(g, gm(Q2T.p, Q2T.bs, nT, 0, QT.at(r1, 0), QT.bs, nR, 0, QT2.p,
+                                           QT2.bs, nR, nT, nR, nT, 1.0, 0.0), s_);
+                            flush(g, s_, 6);
+                        }
+                        CopyBatch cc;
+                        add_copy(cc, cp(DT2.p, DT2.bs, nT, DT.p + r1, DT.bs, nR, c, nT));
+                        add_copy(cc, cp(QT2.p, QT2.bs, nR, QT.at(r1, 0), QT.bs, nR, nT, nR));
+                        flush(cc);
+                        {
+                            Timed tm(this, 6);
+                            CK(launch_tail_rank(DT.p, DT.bs, c, nR, part, d_tol_, d_rank_, d_dropped_,
+                                                nullptr, d_active, s_, st_));
+                        }
+                        for (Blk *b : {&M2, &Q2T, &DT2, &QT2}) release(*b);
+                        st_acc_->launches += 8;
+                    }
+                }
+                CK(cudaFreeAsync(d_r1, st_));
+                st_acc_->launches += 5;
+                std::vector<int> rk(s_), act(s_);
+                std::vector<double> dr(s_);
+                CK(cudaMemcpyAsync(rk.data(), d_rank_, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
+                CK(cudaMemcpyAsync(act.data(), d_active, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
+                CK(cudaMemcpyAsync(dr.data(), d_dropped_, sizeof(double) * s_, cudaMemcpyDeviceToHost, st_));
+                sync();
+                t = 0;
+                dropped = 0.0;
+                for (int z = 0; z < s_; ++z)
+                    if (act[z]) {
+                        t = std::max(t, rk[z]);
+                        dropped += dr[z];
+                    }
+                if (kmax >= nR || t + 8 < kmax) break;
+                kmax = nR;
+            }
+            st_acc_->dropped_fro += dropped;
+            t_level_max_ = std::max(t_level_max_, t);
             st_acc_->recompressions++;
             {   // algorithmic QR of G (nR x c), survey §8d: 2 c nR^2 - 2/3 nR^3 (for c >= nR)
                 const double a = std::max(c, nR), b = std::min(c, nR);

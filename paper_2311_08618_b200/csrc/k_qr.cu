@@ -251,7 +251,7 @@ template <int CS>
 __global__ void __launch_bounds__(PQRC_THREADS) pqr_cluster_kernel(double *Mg, int64_t mstride, int n,
                                                                    double *tau, int *piv,
                                                                    int64_t vstride,
-                                                                   const int *active) {
+                                                                   const int *active, int kmax) {
     // One cluster barrier per column: every CTA proposes its best unused column
     // together with that column's Householder vector (double-buffered by step
     // parity), then all CTAs take the same winner, copy its vector through
@@ -291,7 +291,10 @@ __global__ void __launch_bounds__(PQRC_THREADS) pqr_cluster_kernel(double *Mg, i
     cluster.sync();  // every CTA has read M before any reflector overwrites it
     __shared__ int s_lc, s_win[2];
     __shared__ double s_tau;
-    for (int j = 0; j < n; ++j) {
+    // kmax < n: only the leading kmax pivots are ordered (the recompression keeps a
+    // few dozen directions); Q = H_0 ... H_{kmax-1} still spans R^n, its trailing
+    // columns an unordered orthonormal complement
+    for (int j = 0; j < kmax; ++j) {
         const int par = j & 1;
         double *myv = vb + (size_t)par * n;
         double *mys = slot + 4 * par;
@@ -450,7 +453,7 @@ __global__ void __launch_bounds__(FQ_WARPS * 32) form_q_rows_kernel(const double
                                                                    int n, const double *tau,
                                                                    int64_t tstr, double *QT,
                                                                    int64_t qstr,
-                                                                   const int *active) {
+                                                                   const int *active, int kref) {
     extern __shared__ __align__(16) double ybuf[];
     const int z = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -466,7 +469,7 @@ __global__ void __launch_bounds__(FQ_WARPS * 32) form_q_rows_kernel(const double
     __syncwarp();
     const double *Vz = V + z * vstr;
     const double *tzz = tau + z * tstr;
-    for (int j = min(q, n - 1); j >= 0; --j) {
+    for (int j = min(q, kref - 1); j >= 0; --j) {
         const double *v = Vz + (int64_t)j * n;
         double sdot = (lane == 0) ? y[j] : 0.0;
         for (int r = j + 1 + lane; r < n; r += 32) sdot += v[r] * y[r];
@@ -487,7 +490,8 @@ size_t pqr_cluster_smem(int n, int cs) {
 
 template <int CS>
 cudaError_t launch_pqr_cluster_cs(double *M, int64_t mstride, int n, double *tau, int *piv,
-                                  int64_t vstride, const int *active, int nshift, cudaStream_t st) {
+                                  int64_t vstride, const int *active, int nshift, cudaStream_t st,
+                                  int kmax) {
     const size_t smem = pqr_cluster_smem(n, CS);
     cudaError_t e = smem_optin(pqr_cluster_kernel<CS>);
     if (e != cudaSuccess) return e;
@@ -509,7 +513,8 @@ cudaError_t launch_pqr_cluster_cs(double *M, int64_t mstride, int n, double *tau
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, pqr_cluster_kernel<CS>, M, mstride, n, tau, piv, vstride, active);
+    return cudaLaunchKernelEx(&cfg, pqr_cluster_kernel<CS>, M, mstride, n, tau, piv, vstride, active,
+                              kmax);
 }
 
 }  // namespace
@@ -523,24 +528,27 @@ int pqr_cluster_size(int n) {
 }
 
 cudaError_t launch_pqr_cluster(double *M, int64_t mstride, int n, double *tau, int *piv,
-                               int64_t vstride, const int *active, int nshift, cudaStream_t st) {
+                               int64_t vstride, const int *active, int nshift, cudaStream_t st,
+                               int kmax) {
     if (nshift <= 0 || n <= 0) return cudaSuccess;
+    kmax = kmax <= 0 ? n : std::min(kmax, n);
     const int cs = pqr_cluster_size(n);
-    if (cs == 8) return launch_pqr_cluster_cs<8>(M, mstride, n, tau, piv, vstride, active, nshift, st);
-    if (cs == 16) return launch_pqr_cluster_cs<16>(M, mstride, n, tau, piv, vstride, active, nshift, st);
+    if (cs == 8) return launch_pqr_cluster_cs<8>(M, mstride, n, tau, piv, vstride, active, nshift, st, kmax);
+    if (cs == 16) return launch_pqr_cluster_cs<16>(M, mstride, n, tau, piv, vstride, active, nshift, st, kmax);
     return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_form_q_rows(const double *V, int64_t vstride, int n, const double *tau,
                                int64_t tstride, double *QT, int64_t qstride, const int *active,
-                               int nshift, cudaStream_t st) {
+                               int nshift, cudaStream_t st, int kref) {
     if (nshift <= 0 || n <= 0) return cudaSuccess;
+    kref = kref <= 0 ? n : std::min(kref, n);
     const size_t smem = sizeof(double) * FQ_WARPS * (size_t)n;
     cudaError_t e = smem_optin(form_q_rows_kernel);
     if (e != cudaSuccess) return e;
     dim3 grid((n + FQ_WARPS - 1) / FQ_WARPS, nshift);
     form_q_rows_kernel<<<grid, FQ_WARPS * 32, smem, st>>>(V, vstride, n, tau, tstride, QT, qstride,
-                                                         active);
+                                                         active, kref);
     return cudaGetLastError();
 }
 

@@ -11,18 +11,19 @@ opt = sys.argv[1]
 vals = [int(v) for v in sys.argv[2].split(",")]
 S = int(sys.argv[3]) if len(sys.argv) > 3 else 7
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
-Hd, cloud = gpu_build.config_device(os.environ.get("CFG", "cfg2"))
+nn = int(os.environ["N"]) if "N" in os.environ else None
+Hd, cloud = gpu_build.config_device(os.environ.get("CFG", "cfg2"), n=nn)
 torch.cuda.synchronize()
 eng = _native.engine_for(Hd, 0)
 eng.set_option("max_batch", S)
 eng.set_option("concurrency", 1)
-eng.set_option("time_kernels", 2)
-mus = [-10.0 + 2.0 * q for q in range(S)]
+eng.set_option("time_kernels", int(os.environ.get("TK", "2")))
+mus = [float(os.environ.get("MU0", "-10")) + float(os.environ.get("DMU", "2")) * q for q in range(S)]
 eng.inertia(mus[:1])
 for r in range(reps):
     for v in vals:
         eng.set_option(opt, v)
         counts, status, st = eng.inertia(mus)
-        print(f"rep {r} {opt}={v}: total {st['ms_total']:.0f} ms, schur {st['ms_schur']:.0f} ms "
-              f"({st['schur_flops'] / st['ms_schur'] / 1e9:.1f} TF/s), counts0 {counts[0].tolist()}",
+        print(f"rep {r} {opt}={v}: total {st['ms_total']:.0f} ms, schur {st['ms_schur']:.0f} ms, "
+              f"qr {st['ms_kind'][6]:.0f} ms, rank_added {st['rank_added']}, counts0 {counts[0].tolist()}",
               flush=True)
