@@ -26,6 +26,7 @@
 // the reference carries its (exactly zero) redundant rows through the
 // products (gldl.py:365-409); skipping them changes no value.
 #include <algorithm>
+#include <unordered_map>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -139,6 +140,7 @@ public:
         else if (k == "borrow_arena") borrow_arena_ = v != 0;
         else if (k == "elim_order") elim_order_ = (int)v;
         else if (k == "qr_budget") qr_budget_ = v != 0;
+        else if (k == "block_cache") block_cache_ = v != 0;
         else throw CudaFail(H2L_EINVAL, "unknown option " + k);
     }
 
@@ -282,7 +284,7 @@ public:
         ranges_ = o.ranges_; boff_ = o.boff_; brank_ = o.brank_; bdim_ = o.bdim_;
         dense_ = o.dense_; lowrank_ = o.lowrank_; deferred_ = o.deferred_; coup_off_ = o.coup_off_;
         arena_ = o.arena_; skel_ = o.skel_; skel_diag_ = o.skel_diag_; skel_off_ = o.skel_off_;
-        max_batch_ = o.max_batch_; time_kernels_ = o.time_kernels_; schur_variant_ = o.schur_variant_; elim_order_ = o.elim_order_; qr_budget_ = o.qr_budget_;
+        max_batch_ = o.max_batch_; time_kernels_ = o.time_kernels_; schur_variant_ = o.schur_variant_; elim_order_ = o.elim_order_; qr_budget_ = o.qr_budget_; block_cache_ = o.block_cache_;
         owns_payload_ = false;
         uploaded_ = o.uploaded_;
     }
@@ -539,7 +541,15 @@ private:
                 b.p = base + GUARD;
                 live_[b.p] = inner;
             } else {
-                CK(cudaMallocFromPoolAsync((void **)&b.p, sizeof(double) * b.bs * s_, pool_, st_));
+                const int64_t nd = b.bs * s_;
+                auto it = block_cache_ ? bcache_.find(nd) : bcache_.end();
+                if (it != bcache_.end() && !it->second.empty()) {
+                    b.p = it->second.back();
+                    it->second.pop_back();
+                    bcache_bytes_ -= nd * (int64_t)sizeof(double);
+                } else {
+                    CK(cudaMallocFromPoolAsync((void **)&b.p, sizeof(double) * nd, pool_, st_));
+                }
             }
             if (zero) CK(cudaMemsetAsync(b.p, 0, sizeof(double) * b.bs * s_, st_));
         }
@@ -553,10 +563,29 @@ private:
                 live_.erase(b.p);
                 CK(cudaFreeAsync(b.p - GUARD, st_));
             } else {
-                CK(cudaFreeAsync(b.p, st_));
+                // same-size blocks are re-issued from a host-side free list (one stream:
+                // stream order makes reuse safe); the pool call per block costs more
+                // host time than the kernels of small fronts
+                const int64_t nd = b.bs * s_, by = nd * (int64_t)sizeof(double);
+                if (block_cache_ && bcache_bytes_ + by <= BCACHE_CAP) {
+                    bcache_[nd].push_back(b.p);
+                    bcache_bytes_ += by;
+                } else {
+                    CK(cudaFreeAsync(b.p, st_));
+                }
             }
         }
         b = Blk{};
+    }
+    static constexpr int64_t BCACHE_CAP = int64_t(2) << 30;
+    std::unordered_map<int64_t, std::vector<double *>> bcache_;
+    int64_t bcache_bytes_ = 0;
+    bool block_cache_ = true;
+    void flush_block_cache() {
+        for (auto &kv : bcache_)
+            for (double *p : kv.second) CK(cudaFreeAsync(p, st_));
+        bcache_.clear();
+        bcache_bytes_ = 0;
     }
 
     // -------------------------------------------------- batched task builders
@@ -775,6 +804,7 @@ private:
         offd_.clear();
         coup_.clear();
         fill_.clear();
+        flush_block_cache();
     }
 
     void reset_adjacency(int nclus) {
