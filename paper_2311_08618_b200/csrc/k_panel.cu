@@ -21,6 +21,8 @@
 namespace h2l {
 
 constexpr int PANEL_L_SMEM = 160;
+constexpr int PANEL_LC = 16;  // widest L column chunk staged per pass when L does not fit
+constexpr size_t PANEL_SMEM_CAP = 226 * 1024;
 
 namespace {
 
@@ -69,7 +71,7 @@ __global__ void __launch_bounds__(256) panel_kernel(const PanelTile *tiles, cons
                                                     int64_t lstride, int ldl, int n,
                                                     const int *perm, const double *dinfo,
                                                     int64_t pstride, double *W, double *X,
-                                                    int64_t wstride, int ldw) {
+                                                    int64_t wstride, int ldw, int lcw) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double colbuf[2][PANEL_ROWS];
     const int S = n + 1 + (n & 1);  // odd row stride -> conflict-free column access
@@ -119,14 +121,27 @@ __global__ void __launch_bounds__(256) panel_kernel(const PanelTile *tiles, cons
     else if (lsm && n <= 128) solve_regs<16>(T, S, Ls, cs, n, colbuf);
     else if (lsm) solve_regs<20>(T, S, Ls, cs, n, colbuf);
     else {
-        for (int c = 0; c < n - 1; ++c) {
-            const double wc = trow[c];
-            const bool two = dz[3 * c + 2] > 1.5;
-            for (int cc = c + 1 + warp; cc < n; cc += 8) {
-                const double l = (two && cc == c + 1) ? 0.0 : __ldg(Lz + (int64_t)cc * ldl + c);
-                trow[cc] -= wc * l;
+        // L does not fit: stage it in column chunks of PANEL_LC (rows c0+1..n-1,
+        // row-contiguous, coalesced) and run the same column steps from shared memory
+        double *Lc = T + PANEL_ROWS * S;  // [n][lcw]
+        for (int c0 = 0; c0 < n - 1; c0 += lcw) {
+            const int nc = min(lcw, n - 1 - c0);
+            __syncthreads();
+            for (int e = threadIdx.x; e < (n - c0) * lcw; e += blockDim.x) {
+                const int i = c0 + e / lcw, k = e % lcw;
+                Lc[(int64_t)i * lcw + k] = (k < nc && i > c0 + k) ? Lz[(int64_t)i * ldl + c0 + k] : 0.0;
             }
             __syncthreads();
+            for (int k = 0; k < nc; ++k) {
+                const int c = c0 + k;
+                const double wc = trow[c];
+                const bool two = dz[3 * c + 2] > 1.5;
+                for (int cc = c + 1 + warp; cc < n; cc += 8) {
+                    const double l = (two && cc == c + 1) ? 0.0 : Lc[(int64_t)cc * lcw + k];
+                    trow[cc] -= wc * l;
+                }
+                __syncthreads();
+            }
         }
     }
 
@@ -153,9 +168,18 @@ __global__ void __launch_bounds__(256) panel_kernel(const PanelTile *tiles, cons
 
 }  // namespace
 
+// width of the staged L chunk for n > PANEL_L_SMEM (the widest that fits)
+int panel_lcw(int n) {
+    int w = PANEL_LC;
+    while (w > 1 && sizeof(double) * ((size_t)PANEL_ROWS * (n + 2) + (size_t)n * w) > PANEL_SMEM_CAP)
+        w >>= 1;
+    return w;
+}
+
 size_t panel_smem_bytes(int n) {
     size_t b = sizeof(double) * PANEL_ROWS * (size_t)(n + 2);
     if (n <= PANEL_L_SMEM) b += sizeof(double) * (size_t)n * (n - 1) / 2 + sizeof(int) * (size_t)n;
+    else b += sizeof(double) * (size_t)n * panel_lcw(n);
     return b;
 }
 
@@ -170,7 +194,7 @@ cudaError_t launch_panel(const PanelTile *dev_tiles, int ntiles, int nshift, con
     if (e != cudaSuccess) return e;
     dim3 grid(ntiles, nshift);
     panel_kernel<<<grid, 256, sm, st>>>(dev_tiles, L, lstride, ldl, n, perm, dinfo, pstride, W, X,
-                                        wstride, ldw);
+                                        wstride, ldw, panel_lcw(n));
     return cudaGetLastError();
 }
 
