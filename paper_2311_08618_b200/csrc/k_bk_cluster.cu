@@ -190,7 +190,10 @@ __global__ void __launch_bounds__(BKC_THREADS) bk_cluster_kernel(const BkJob *jo
         }
         const int kk = k + kstep - 1;
         if (tid == 0) { swaps[2 * k] = kk; swaps[2 * k + 1] = kp; }
-        cl.sync();  // every decision input has been read
+        // without an interchange nothing the other CTAs may still read (column k,
+        // the owner's arg-max slot) is written before the end-of-step barrier, so
+        // the two interchange barriers are skipped (kp, kk are cluster-uniform)
+        if (kp != kk) cl.sync();  // every decision input has been read
         // ---- interchange kk <-> kp on the lower triangle (owner of column kk)
         if (kp != kk && A.mine(kk)) {
             for (int i = kp + 1 + tid; i < n; i += nthr) {
@@ -211,7 +214,7 @@ __global__ void __launch_bounds__(BKC_THREADS) bk_cluster_kernel(const BkJob *jo
             }
         }
         if (kp != kk && crank == 0 && tid == 0) { const int q = perm[kk]; perm[kk] = perm[kp]; perm[kp] = q; }
-        cl.sync();
+        if (kp != kk) cl.sync();
         // ---- pivot columns into every CTA
         {
             const double *src = A.rem(cl, k, k);
