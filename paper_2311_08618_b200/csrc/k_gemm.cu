@@ -58,10 +58,15 @@ template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 template <int BM_, int BN_, int WM_, int WN_, int STAGES_, bool CSTAGE_ = true, int MINB_ = 1,
-          int BK_ = 16>
+          int BK_ = 16, bool KP_ = false>
 struct GemmCfg {
     static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_;
-    static constexpr int BK = BK_, SK = BK_ + 4;  // K chunk; padded shared row (conflict-free)
+    // KP: k permuted inside a 16-chunk (position (k % 4) * 4 + k / 4) so a lane's
+    // fragments of the 4 DMMA k-steps are contiguous: 2 LDS.128 instead of 4
+    // LDS.64 per fragment; row stride 18 keeps the 128-bit loads conflict-free
+    static constexpr bool KP = KP_;
+    static_assert(!KP_ || BK_ == 16, "k permutation defined for 16-chunks");
+    static constexpr int BK = BK_, SK = KP_ ? BK_ + 2 : BK_ + 4;  // K chunk; padded shared row
     static constexpr bool CSTAGE = CSTAGE_;  // prefetch C into shared memory
     static constexpr int MINB = MINB_;       // min resident CTAs per SM (register cap)
     static constexpr int WARPS = (BM / WM) * (BN / WN);
@@ -77,8 +82,9 @@ struct GemmCfg {
 // e = tid + q*THREADS (q < ROWS*16/THREADS) of every chunk; their global and
 // shared addresses differ by fixed strides, so the pointers, row predicates
 // and shared offsets are computed once per tile and each chunk costs one add.
-template <int ROWS, int THREADS, int BK, int SK>
+template <int ROWS, int THREADS, int BK, int SK, bool KP = false>
 struct Loader {
+    static __device__ __forceinline__ int kpos(int k) { return KP ? (k & 3) * 4 + (k >> 2) : k; }
     static_assert(THREADS % ROWS == 0 && THREADS % BK == 0, "loader layout");
     static constexpr int NQ = ROWS * BK / THREADS;
     const double *p;        // element q = 0 of chunk 0
@@ -98,8 +104,8 @@ struct Loader {
             p = X + (int64_t)kl0 * ld + row0 + rl0;
             dq = (int64_t)kstep * ld; dk = (int64_t)BK * ld;
         }
-        soff = (unsigned)((rl0 * SK + kl0) * sizeof(double));
-        sdq = (unsigned)((rstep * SK + kstep) * sizeof(double));
+        soff = (unsigned)((rl0 * SK + kpos(kl0)) * sizeof(double));
+        sdq = (unsigned)((rstep * SK + kstep) * sizeof(double));  // KP: trans uses kpos per q
         rowok = 0;
 #pragma unroll
         for (int q = 0; q < NQ; ++q) rowok |= (row0 + rl0 + q * rstep < rows) ? (1u << q) : 0u;
@@ -111,9 +117,12 @@ struct Loader {
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
             const bool ok = ((rowok >> q) & 1u) && (kl0 + q * kstep < krem);
+            const unsigned so = (KP && kstep)
+                ? soff + (unsigned)((kpos(kl0 + q * kstep) - kpos(kl0)) * sizeof(double))
+                : soff + q * sdq;
             // src-size 0 (zero fill) reads nothing, so the address needs no clamp
             asm volatile("cp.async.ca.shared.global.L2::128B [%0], [%1], 8, %2;\n"
-                         ::"r"(sbase + soff + q * sdq), "l"(pc + q * dq), "r"(ok ? 8 : 0));
+                         ::"r"(sbase + so), "l"(pc + q * dq), "r"(ok ? 8 : 0));
         }
     }
 };
@@ -136,8 +145,8 @@ __device__ __forceinline__ void tile_mainloop(const double *A, int lda, int tA, 
 #pragma unroll
         for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     const int nk = (K + BK - 1) / BK;
-    const Loader<BM, THREADS, BK, SK> la(A, lda, tA, M, m0, tid);
-    const Loader<BN, THREADS, BK, SK> lb(B, ldb, b_trans, N, n0, tid);
+    const Loader<BM, THREADS, BK, SK, Cfg::KP> la(A, lda, tA, M, m0, tid);
+    const Loader<BN, THREADS, BK, SK, Cfg::KP> lb(B, ldb, b_trans, N, n0, tid);
     const unsigned sA = (unsigned)__cvta_generic_to_shared(&As[0][0][0]);
     const unsigned sB = (unsigned)__cvta_generic_to_shared(&Bs[0][0][0]);
     constexpr unsigned SA_STAGE = BM * SK * sizeof(double), SB_STAGE = BN * SK * sizeof(double);
@@ -160,6 +169,29 @@ __device__ __forceinline__ void tile_mainloop(const double *A, int lda, int tA, 
         }
         cp_commit();
         const int cur = kc % STAGES;
+        if constexpr (Cfg::KP) {
+            // same accumulation order as below (k-steps 0, 4, 8, 12): bitwise identical
+#pragma unroll
+            for (int hp = 0; hp < 2; ++hp) {
+                double2 af[FM], bf[FN];
+#pragma unroll
+                for (int i = 0; i < FM; ++i)
+                    af[i] = *reinterpret_cast<const double2 *>(
+                        &As[cur][wm + i * 8 + (lane >> 2)][(lane & 3) * 4 + 2 * hp]);
+#pragma unroll
+                for (int j = 0; j < FN; ++j)
+                    bf[j] = *reinterpret_cast<const double2 *>(
+                        &Bs[cur][wn + j * 8 + (lane >> 2)][(lane & 3) * 4 + 2 * hp]);
+#pragma unroll
+                for (int i = 0; i < FM; ++i)
+#pragma unroll
+                    for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i].x, bf[j].x);
+#pragma unroll
+                for (int i = 0; i < FM; ++i)
+#pragma unroll
+                    for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i].y, bf[j].y);
+            }
+        } else {
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 4) {
             double af[FM], bf[FN];
@@ -171,6 +203,7 @@ __device__ __forceinline__ void tile_mainloop(const double *A, int lda, int tA, 
             for (int i = 0; i < FM; ++i)
 #pragma unroll
                 for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
         }
     }
     cp_wait<0>();
@@ -490,9 +523,11 @@ int schur_sym_tiles(int R) {
 // variants (engine option "schur_variant"; tools/ab_option.py): 0 production
 // (epilogue as fire-and-forget L2 reductions, RED.ADD.F64: 9 % faster than 4),
 // 1 + L2 prefetch of the targets, 2 three-stage pipeline at 3 CTAs/SM,
-// 3 K chunks of 32 at 3 CTAs/SM, 4 load / subtract / store epilogue
+// 3 K chunks of 32 at 3 CTAs/SM, 4 load / subtract / store epilogue,
+// 5 k-permuted tiles read with 128-bit shared loads (within noise of 0)
 using SymV2 = GemmCfg<64, 64, 32, 32, 3, false, 3>;
 using SymV3 = GemmCfg<64, 64, 32, 32, 2, false, 3, 32>;
+using SymKP = GemmCfg<64, 64, 32, 32, 2, false, 4, 16, true>;
 
 template <class Cfg, int PF>
 static void launch_sym(const double *X, const double *Bg, int64_t sx, int ld, int R, int K,
@@ -514,6 +549,7 @@ void launch_schur_sym(const double *X, const double *Bg, int64_t sx, int ld, int
         case 2: launch_sym<SymV2, 0>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, tiles, nshift, st); break;
         case 3: launch_sym<SymV3, 0>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, tiles, nshift, st); break;
         case 4: launch_sym<Prod, 0>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, tiles, nshift, st); break;
+        case 5: launch_sym<SymKP, 2>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, tiles, nshift, st); break;
         default: launch_sym<Prod, 2>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, tiles, nshift, st);
     }
 }

@@ -303,7 +303,7 @@ def test_engine_options_keep_counts(option):
     variants) never change the inertia: counts equal the reference's with the
     option off and on, on instances with recompression and merges."""
     names = [n for n in instance_names() if n.startswith("mini")] + ["circle256_h2_e8"]
-    values = {"qr_budget": (0, 1), "block_cache": (0, 1), "schur_variant": (1, 2, 3, 4, 0)}[option]
+    values = {"qr_budget": (0, 1), "block_cache": (0, 1), "schur_variant": (1, 2, 3, 4, 5, 0)}[option]
     for name in names:
         H = h2matrix.load_payload(f"tests/golden/h_{name}.npz")
         z = golden(f"counts_{name}.npz")
