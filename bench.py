@@ -301,8 +301,12 @@ def run_ours(args):
     H = wl.H
     S = args.batch or {"cfg1": 255, "cfg2": 7, "cfg4": 2}.get(wl.name, 15)
     eng = _native.engine_for(H, local)
-    eng.set_option("max_batch", S)
-    eng.set_option("concurrency", 1)
+    # latency-bound configs overlap two waves' per-cluster chains (tools/conc_sweep.py:
+    # config 3 0.24 vs 0.27 s per shift); config 2 is memory- and DMMA-bound
+    conc = 2 if wl.name in ("cfg3", "cfg5") else 1
+    eng.set_option("max_batch", (S + conc - 1) // conc)
+    eng.set_option("concurrency", conc)
+    wl.config["waves"] = f"{conc} concurrent wave(s) of <= {(S + conc - 1) // conc} shifts"
     if wl.name == "cfg4":
         # the unit-sphere front does not fit one B200 in the reference's ascending
         # order; low-degree-first keeps a shift at ~45 GB (counts are order-free)
