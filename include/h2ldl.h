@@ -131,7 +131,11 @@ int h2l_inertia(h2l_engine *engine, const double *mu, int32_t s, int64_t *counts
  * 0 off, 1 CUDA-event timing of every launch kind (stats.ms_kind), 2 the Schur
  * GEMM launches only (stats.ms_schur; negligible overhead); "borrow_arena" 1:
  * a device-resident plan arena is used in place by h2l_upload instead of being
- * copied (it must then outlive the engine); "schur_variant" kernel variant (0).
+ * copied (it must then outlive the engine); "schur_variant" Schur kernel
+ * variant (0 production); "elim_order" 0 ascending (the reference), 1 low
+ * near-field degree first (smaller fronts; counts unchanged); "qr_budget" 1/0
+ * budgeted recompression ordering; "block_cache" 1/0 host free list of blocks.
+ * Unknown keys fail with H2L_EINVAL.
  */
 int h2l_set_option(h2l_engine *engine, const char *key, int64_t value);
 
