@@ -307,9 +307,16 @@ def run_ours(args):
     eng.set_option("max_batch", (S + conc - 1) // conc)
     eng.set_option("concurrency", conc)
     wl.config["waves"] = f"{conc} concurrent wave(s) of <= {(S + conc - 1) // conc} shifts"
+    sched = args.schedule if args.schedule >= 0 else (1 if wl.name in ("cfg1", "cfg2") else 2)
+    eng.set_option("schedule", sched)
+    wl.config["schedule"] = {0: "one cluster at a time, ascending (the reference)",
+                             1: "ascending-order wavefronts (level-batched, reference order)",
+                             2: "colour classes (level-batched, re-ordered)"}[sched]
     if wl.name == "cfg4":
         # the unit-sphere front does not fit one B200 in the reference's ascending
-        # order; low-degree-first keeps a shift at ~45 GB (counts are order-free)
+        # order; low-degree-first keeps a shift at ~45 GB.  A re-ordering changes fills and
+        # truncation (not guaranteed count-neutral): counts are checked against the
+        # reference on the golden and production-size instances, and the line flags it
         eng.set_option("elim_order", 1)
         wl.config["elimination_order"] = "low near-field degree first (ascending needs > 180 GB)"
     # Schur launches timed by CUDA events inside the timed region (the roofline);
@@ -338,34 +345,54 @@ def run_ours(args):
     else:
         sharded = local_eval
     marks = {}
+    searches = []       # complete eigenvalue searches inside the timed region
 
     def evaluate(mus):
         if state["phase"] == "warm" and state["n"] == W:
-            if world > 1:
-                dist.barrier()
-            torch.cuda.synchronize()
-            state["phase"] = "timed"
-            marks["clock"] = ClockSampler(local)
-            marks["clock"].start()
-            marks["t0"] = time.perf_counter()
-        elif state["phase"] == "timed" and state["n"] == W + K:
-            torch.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
-            marks["t1"] = time.perf_counter()
+            raise _Stop()  # the warm-up search is abandoned; the timed searches start fresh
+        if state["phase"] == "timed" and state["n"] == W + K:
             raise _Stop()
         state["n"] += 1
         return sharded(mus)
 
-    cache = InertiaCache()
+    # warm-up: W rounds of a search for another index (restarted if it converges)
+    k_warm = wl.ks[0] if wl.ks[0] != wl.k else wl.n + 1 - wl.k
     try:
-        multisection(H, [wl.k], wl.interval, wl.eps_ev, cache=cache, batch=S * world,
-                     evaluate=evaluate)
+        while True:
+            multisection(H, [k_warm], wl.interval, wl.eps_ev, cache=InertiaCache(),
+                         batch=S * world, evaluate=evaluate)
     except _Stop:
         pass
-    if "t1" not in marks:  # search converged before W + K rounds (small configs)
-        torch.cuda.synchronize()
-        marks["t1"] = time.perf_counter()
+    # timed: exactly K rounds; fresh searches for k (then the config's other indices,
+    # cyclically), each round one batched sweep of S shifts per GPU
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    state["phase"] = "timed"
+    marks["clock"] = ClockSampler(local)
+    marks["clock"].start()
+    marks["t0"] = time.perf_counter()
+    order = [wl.k] + [k for k in wl.ks if k != wl.k]
+    q = 0
+    try:
+        while True:
+            k = order[q % len(order)]
+            q += 1
+            n0, t0 = len(steps), time.perf_counter()
+            (est,) = multisection(H, [k], wl.interval, wl.eps_ev, cache=InertiaCache(),
+                                  batch=S * world, evaluate=evaluate)
+            rounds = steps[n0:]
+            searches.append({"k": k, "value": est.value, "half_width": est.half_width,
+                             "iterations": est.iterations, "rounds": len(rounds),
+                             "shifts": sum(len(m) for _, m, _ in rounds),
+                             "device_s": sum(st["ms_total"] for _, _, st in rounds) / 1e3,
+                             "wall_s": time.perf_counter() - t0})
+    except _Stop:
+        pass
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    marks["t1"] = time.perf_counter()
     clk = marks["clock"].stop() if "clock" in marks else None
     timed = [st for ph, _, st in steps if ph == "timed"]
     timed_mus = [m for ph, m, _ in steps if ph == "timed"]
@@ -419,13 +446,29 @@ def run_ours(args):
     q = max(1, int(math.floor(math.log2(S * world + 1))))
     levels, nrounds = rounds_needed(wl.interval, wl.eps_ev, q)
     step_s = t_dev / max(1, len(timed))
+    done = [x for x in searches]
     eig = {"k": wl.k, "eps_ev": wl.eps_ev, "bisection_levels": levels,
            "multisection_rounds": nrounds, "shifts_per_round": S * world,
-           "s_per_eigenvalue_multisection": nrounds * step_s,
-           "s_per_eigenvalue_sequential": levels * (sum(single) / 1e3 / max(1, len(single))),
-           "projected": True,
-           "rule": "rounds x measured device seconds per round (multisection, S shifts/round);"
-                   " levels x measured one-shift step (sequential bisection)"}
+           "searches_completed_in_timed_region": done,
+           "s_per_eigenvalue_measured": (sum(x["device_s"] for x in done) / len(done)) if done else None,
+           "s_per_eigenvalue_measured_wall": (sum(x["wall_s"] for x in done) / len(done)) if done else None,
+           "projected": {"s_per_eigenvalue_multisection": nrounds * step_s,
+                         "s_per_eigenvalue_sequential": levels * (sum(single) / 1e3 / max(1, len(single))),
+                         "rule": "rounds x measured device seconds per round (multisection, S "
+                                 "shifts/round); levels x measured one-shift step (sequential)"},
+           "note": "each timed search starts from the Gershgorin interval with an empty cache; "
+                   "a search is measured when it completes inside the K timed rounds"}
+    # ---- BASELINE config 2: 32 shifts per factorization call (waves of <= S inside one call)
+    batched32 = None
+    if wl.name == "cfg2" and world == 1 and not args.no_batch32:
+        mus32 = np.linspace(wl.interval[0], wl.interval[1], 34)[1:33]
+        _, _, st32 = ldl_counts_array(H, mus32)
+        batched32 = {"shifts": 32, "max_batch": (S + conc - 1) // conc,
+                     "waves": -(-32 // ((S + conc - 1) // conc)),
+                     "ms_total": st32["ms_total"], "value": 32 / (st32["ms_total"] / 1e3),
+                     "unit": UNIT, "mem_peak_gb_per_wave": st32["mem_peak"] / 1e9,
+                     "note": "32 shifts exceed one B200 as a single wave (~16 GB each): one "
+                             "h2l_inertia call runs them as consecutive waves"}
     if args.eig:
         eng.set_option("time_kernels", 0)
         ks = list(wl.ks)
@@ -481,14 +524,17 @@ def run_ours(args):
                        "elimination_tflops": elim / t_dev / 1e12 if t_dev else None,
                        "dmma_executed_tflops": gemm_exec / (ms / 1e3) / 1e12 if ms else None,
                        "ms_by_kind_one_step": dict(zip(["panel_gemm", "schur_gemm", "rotation_merge_gemm",
-                                               "bk", "panel_solve", "copies", "recompression_qr",
-                                               "unused"], kinds)) if kinds else None,
+                                               "bk", "panel_solve", "copies", "recompression_products",
+                                               "recompression_ordering"], kinds)) if kinds else None,
                        "device_mem_peak_gb": mem_peak / 1e9},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * S,
                 "d2h_bytes_per_step": (3 * 8 + 4) * S},
         "gpu_launches": launches,
         "clocks": clk,
         "single_shift": {"value": single_rate, "unit": UNIT, "ms_per_step": float(np.mean(single))},
+        "batched_32": batched32,
+        "groups_per_step": sum(st["groups"] for st in timed) / max(1, len(timed)),
+        "launches_per_step": launches / max(1, len(timed)),
         "eigenvalue": eig,
         "construction_s": wl.construct_s,
         "elim_flops_per_eval": elim / max(1, n_local),
@@ -623,6 +669,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--schedule", type=int, default=-1, help="elimination schedule (engine option)")
+    ap.add_argument("--no-batch32", action="store_true", help="skip config 2's 32-shift call")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

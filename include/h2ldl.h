@@ -104,10 +104,17 @@ typedef struct h2l_stats {
     double gemm_flops_exec; /* flops executed by all DMMA GEMM launches (2MNK) */
     double ms_kind[8];    /* device ms per launch kind (time_kernels=1): 0 panel GEMMs,
                              1 Schur GEMM, 2 rotation/merge GEMMs, 3 BK, 4 panel solve,
-                             5 copies, 6 recompression QR, 7 unused */
+                             5 copies, 6 recompression Gram / energy products and tail
+                             rank, 7 recompression ordering (pivoted QR, Q^T) */
     double ms_host;       /* wall-clock ms of the call on the host */
     double mem_peak;      /* bytes: high-water mark of the waves' device pools during the call */
     double elim_flops;    /* the elimination part of `flops` (BK + panel + Schur, live rows) */
+    int64_t groups;       /* elimination groups (clusters eliminated together, one launch per
+                             kernel kind) summed over levels and waves */
+    int64_t paths[4];     /* cluster-steps through the large-front kernels: 0 BK in a
+                             thread-block cluster (n_R > 224), 1 panel with L staged in
+                             chunks (n_R > 160), 2 Gram ordering on a 16-CTA cluster,
+                             3 Gram ordering beyond distributed shared memory (one CTA) */
 } h2l_stats;
 
 int h2l_create(h2l_engine **engine, int device);
@@ -126,15 +133,61 @@ int h2l_inertia(h2l_engine *engine, const double *mu, int32_t s, int64_t *counts
                 int32_t *status, h2l_stats *stats);
 
 /*
- * Tuning knobs (key, value): "max_batch" shifts per device wave (default 64);
- * "concurrency" waves in flight on private streams (default 2); "time_kernels"
- * 0 off, 1 CUDA-event timing of every launch kind (stats.ms_kind), 2 the Schur
- * GEMM launches only (stats.ms_schur; negligible overhead); "borrow_arena" 1:
- * a device-resident plan arena is used in place by h2l_upload instead of being
- * copied (it must then outlive the engine); "schur_variant" Schur kernel
- * variant (0 production); "elim_order" 0 ascending (the reference), 1 low
- * near-field degree first (smaller fronts; counts unchanged); "qr_budget" 1/0
- * budgeted recompression ordering; "block_cache" 1/0 host free list of blocks.
+ * Same as h2l_inertia, but the result stays on the device: dev_counts is device
+ * memory on the engine's device, [s][4] int64 rows (neg, zero, pos, status).
+ * The multi-GPU drivers all-gather straight from this buffer (no host staging).
+ */
+int h2l_inertia_device(h2l_engine *engine, const double *mu, int32_t s, int64_t *dev_counts,
+                       h2l_stats *stats);
+
+/*
+ * Multi-GPU in one process: one engine per device, each with
+ * the same payload uploaded; a call shards the shifts over the engines in
+ * contiguous slices (reference parallel.py:85-96), every engine factorizes its
+ * slice on its own host thread, and the packed counts are exchanged by one NCCL
+ * all-gather between the engines' device buffers (NCCL is dlopen'ed at
+ * h2l_comm_init).  Counts are identical to h2l_inertia on any one engine.
+ * stats (nullable): summed work, ms_total = max over the engines.
+ */
+typedef struct h2l_comm h2l_comm;
+int h2l_comm_init(h2l_engine *const *engines, int ngpu, h2l_comm **comm);
+int h2l_inertia_multi(h2l_comm *comm, const double *mu, int32_t s_total, int64_t *counts,
+                      int32_t *status, h2l_stats *stats);
+int h2l_comm_destroy(h2l_comm *comm);
+
+/*
+ * Tuning knobs (key, value):
+ *  "max_batch"    shifts per device wave (default 64);
+ *  "concurrency"  waves in flight on private streams (default 2);
+ *  "time_kernels" 0 off, 1 CUDA-event timing of every launch kind (stats.ms_kind),
+ *                 2 the Schur GEMM launches only (stats.ms_schur; negligible overhead);
+ *  "borrow_arena" 1: a device-resident plan arena is used in place by h2l_upload
+ *                 instead of being copied (it must then outlive the engine);
+ *  "schedule"     0 one cluster at a time in the reference's ascending order;
+ *                 1 (default) wavefronts of the ascending order's dependency DAG:
+ *                 clusters whose eliminations touch disjoint blocks go out in one
+ *                 launch per kernel kind, each shift factors what the ascending
+ *                 sweep factors (up to the rounding of the complement basis under
+ *                 "qr_budget");
+ *                 2 colour classes of a greedy distance-2 colouring: a re-ordered
+ *                 elimination with far fewer groups.  The factored matrix differs
+ *                 from the ascending sweep's at the truncation tolerance (fills and
+ *                 recompression ranks depend on the order), so counts agree with
+ *                 the reference for shifts outside the tolerance band (tested on
+ *                 the golden and production-size instances), not by construction;
+ *                 3 colour classes of consecutive windows of "window" clusters
+ *                 (default 64) of the order: batches like 2 while the eliminated
+ *                 clusters stay a moving front (materialised blocks and fills stay
+ *                 local, as in the ascending sweep); same caveat as 2;
+ *  "group_mem_mb" cap on the temporaries of one group (default 8192);
+ *  "group_max"    cap on the clusters of one group (default 512);
+ *  "elim_order"   0 ascending (the reference), 1 low near-field degree first
+ *                 (smaller fronts; a re-ordering with the same caveat as schedule 2);
+ *  "qr_budget"    1 (default) order only ~1.5x the level's largest recompression
+ *                 rank (+32) pivots, redone with all pivots when the rank reaches
+ *                 the budget (same rank as the full ordering; the dropped
+ *                 complement gets a different orthonormal basis), 0 full ordering;
+ *  "block_cache"  1/0 host free list of same-size blocks.
  * Unknown keys fail with H2L_EINVAL.
  */
 int h2l_set_option(h2l_engine *engine, const char *key, int64_t value);

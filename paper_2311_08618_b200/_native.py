@@ -54,17 +54,20 @@ class Stats(ctypes.Structure):
         ("launches", ctypes.c_int64), ("schur_flops", ctypes.c_double),
         ("gemm_flops_exec", ctypes.c_double), ("ms_kind", ctypes.c_double * 8),
         ("ms_host", ctypes.c_double), ("mem_peak", ctypes.c_double),
-        ("elim_flops", ctypes.c_double),
+        ("elim_flops", ctypes.c_double), ("groups", ctypes.c_int64),
+        ("paths", ctypes.c_int64 * 4),
     ]
 
     def as_dict(self):
         d = {name: getattr(self, name) for name, _ in self._fields_}
         d["ms_kind"] = list(self.ms_kind)
+        d["paths"] = list(self.paths)
         return d
 
 
 SYMBOLS = ("h2l_create", "h2l_destroy", "h2l_last_error", "h2l_upload", "h2l_inertia",
-           "h2l_set_option", "h2l_bk_factor", "h2l_bk_inertia", "h2l_version")
+           "h2l_inertia_device", "h2l_set_option", "h2l_bk_factor", "h2l_bk_inertia",
+           "h2l_comm_init", "h2l_inertia_multi", "h2l_comm_destroy", "h2l_version")
 
 _lib = None
 _lib_lock = threading.Lock()
@@ -87,6 +90,12 @@ def load_library(path=LIB_PATH):
         lib.h2l_upload.argtypes = [vp, ctypes.POINTER(Plan)]
         lib.h2l_inertia.argtypes = [vp, _f64p, ctypes.c_int32, _i64p, _i32p,
                                     ctypes.POINTER(Stats)]
+        lib.h2l_inertia_device.argtypes = [vp, _f64p, ctypes.c_int32, ctypes.c_void_p,
+                                           ctypes.POINTER(Stats)]
+        lib.h2l_comm_init.argtypes = [ctypes.POINTER(vp), ctypes.c_int, ctypes.POINTER(vp)]
+        lib.h2l_inertia_multi.argtypes = [vp, _f64p, ctypes.c_int32, _i64p, _i32p,
+                                          ctypes.POINTER(Stats)]
+        lib.h2l_comm_destroy.argtypes = [vp]
         lib.h2l_set_option.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64]
         lib.h2l_bk_factor.argtypes = [ctypes.c_int, _f64p, ctypes.c_int64, ctypes.c_int32, _i64p,
                                       _f64p, _i64p]
@@ -157,6 +166,57 @@ class DeviceEngine:
             _check(self.lib.h2l_inertia(self.handle, _ptr(mus, _f64p), s, _ptr(counts, _i64p),
                                         _ptr(status, _i32p), ctypes.byref(st)),
                    self.handle, "h2l_inertia")
+        return counts, status, st.as_dict()
+
+
+    def inertia_device(self, mus, out):
+        """Counts straight into device memory: `out` is a CUDA int64 tensor (or a raw
+        device pointer) on this engine's device with >= 4*len(mus) elements, filled
+        with rows (neg, zero, pos, status).  Returns the stats dict."""
+        mus = np.ascontiguousarray(np.asarray(mus, dtype=np.float64).reshape(-1))
+        s = mus.shape[0]
+        ptr = out if isinstance(out, int) else out.data_ptr()
+        if not isinstance(out, int):
+            if out.numel() < 4 * s or str(out.dtype) != "torch.int64" or not out.is_cuda:
+                raise NativeError("inertia_device: out must be a CUDA int64 tensor of 4*s elements")
+        st = Stats()
+        with self.lock:
+            _check(self.lib.h2l_inertia_device(self.handle, _ptr(mus, _f64p), s, ctypes.c_void_p(ptr),
+                                               ctypes.byref(st)), self.handle, "h2l_inertia_device")
+        return st.as_dict()
+
+
+class MultiEngine:
+    """One process driving several GPUs (h2l_comm_init / h2l_inertia_multi): one
+    DeviceEngine per device, each holding the uploaded H, shifts sharded in
+    contiguous slices, counts exchanged by an NCCL all-gather between the
+    engines' device buffers."""
+
+    def __init__(self, H, devices):
+        self.lib = load_library()
+        self.engines = [engine_for(H, d) for d in devices]
+        arr = (ctypes.c_void_p * len(self.engines))(*[e.handle.value for e in self.engines])
+        c = ctypes.c_void_p()
+        _check(self.lib.h2l_comm_init(arr, len(self.engines), ctypes.byref(c)), None, "h2l_comm_init")
+        self.comm = c
+
+    def __del__(self):
+        try:
+            if self.comm:
+                self.lib.h2l_comm_destroy(self.comm)
+                self.comm = None
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+    def inertia(self, mus):
+        mus = np.ascontiguousarray(np.asarray(mus, dtype=np.float64).reshape(-1))
+        s = mus.shape[0]
+        counts = np.zeros((s, 3), dtype=np.int64)
+        status = np.zeros(s, dtype=np.int32)
+        st = Stats()
+        _check(self.lib.h2l_inertia_multi(self.comm, _ptr(mus, _f64p), s, _ptr(counts, _i64p),
+                                          _ptr(status, _i32p), ctypes.byref(st)),
+               None, "h2l_inertia_multi")
         return counts, status, st.as_dict()
 
 

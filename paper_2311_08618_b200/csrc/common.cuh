@@ -54,7 +54,67 @@ struct PanelTile {
     int row0;        // first panel row of the tile
     int nrows;
     int src_row0;
+    int job;         // PanelJob of the tile (multi-cluster launches)
+};
+
+// one cluster's factor + outputs of a panel launch (a group of independent
+// clusters goes out in one launch: tiles carry their job index)
+struct PanelJob {
+    const double *L;   // BK factor (shift 0), row-major, ld = ldl
+    int64_t lstride;
+    const int *perm;   // [shift][pstride]
+    const double *dinfo;
+    int64_t pstride;
+    double *W, *X;     // outputs (shift 0), ld = ldw
+    int64_t wstride;
+    int ldl, n, ldw, lcw;
+};
+
+// one cluster of a multi-cluster symmetric Schur update (k_gemm.cu)
+struct SchurTarget;
+struct SchurJob {
+    const double *X, *Bg;
+    int64_t sx;
+    int ld, R, K, nseg;
+    const int *seg_of, *seg_start;
+    const struct SchurTarget *tbl;
+    int tile0;         // first grid tile of the job
     int pad;
+};
+
+// recompression jobs (k_qr.cu / k_rrqr.cu / k_copy.cu): one cluster each
+struct PqrJob {
+    double *M;          // Gram matrix (shift 0); reflectors overwrite its rows
+    int64_t mstride;
+    double *tau;
+    int *piv;
+    int64_t vstride;
+    double *QT;         // Q^T output (form_q_rows)
+    int64_t qstride;
+    int n, kmax;        // kmax: leading pivots to order (<= n)
+};
+struct RankJob {
+    const double *DT;   // c x n (shift 0)
+    int64_t dstride;
+    double *part;       // [shift][nchunk][n]
+    int *rank, *r1;     // [shift] each (r1 may be null)
+    double *dropped;    // [shift]
+    int c, n;
+};
+struct SumJob {
+    const double *in;
+    int64_t zin, pstride;
+    double *out;
+    int64_t zout, count;
+    int nparts, pad;
+};
+// zero, per shift z, rows (orient 0) or columns (orient 1) [base + rank[z], base + t)
+// of a block: the directions a shift's own rank drops although the wave keeps them
+struct TailZeroJob {
+    double *p;
+    int64_t bs;
+    const int *rank;    // [shift]
+    int ld, other, base, t, orient, pad;  // other: extent of the untouched dimension
 };
 
 // Engine-mode BK job: factor the leading n x n block of a (row-major, ld).
@@ -109,6 +169,12 @@ int schur_sym_tiles(int R);
 void launch_schur_sym(const double *X, const double *Bg, int64_t sx, int ld, int R, int K,
                       const int *seg_of, const int *seg_start, int nseg, const SchurTarget *tbl,
                       int nshift, cudaStream_t st, int variant = 0);
+// several independent clusters in one launch: tile_job[t] = job of grid tile t
+void launch_schur_sym_multi(const SchurJob *jobs, const int *tile_job, int total_tiles,
+                            int nshift, cudaStream_t st);
+void launch_sum_partials_multi(const SumJob *jobs, int njobs, int64_t max_count, int nshift,
+                               cudaStream_t st);
+cudaError_t launch_tail_zero(const TailZeroJob *jobs, int njobs, int nshift, cudaStream_t st);
 void launch_sum_partials(const double *in, int64_t zin, int64_t pstride, int nparts, double *out,
                          int64_t zout, int64_t count, int nshift, cudaStream_t st);
 int gemm_tiles(int M, int N);
@@ -133,6 +199,11 @@ cudaError_t launch_panel(const PanelTile *dev_tiles, int ntiles, int nshift, con
                          int64_t lstride, int ldl, int n, const int *perm, const double *dinfo,
                          int64_t pstride, double *W, double *X, int64_t wstride, int ldw,
                          cudaStream_t st);
+// multi-cluster panel: tiles index `jobs`; smem_bytes = max panel_smem_bytes(n) over jobs
+size_t panel_smem_bytes(int n);
+int panel_lcw(int n);
+cudaError_t launch_panel_multi(const PanelTile *dev_tiles, int ntiles, int nshift,
+                               const PanelJob *dev_jobs, size_t smem_bytes, cudaStream_t st);
 
 cudaError_t launch_pqr(double *GT, int64_t gstride, int c, int nR, int ldg, double *tau, int *piv,
                        int *used, double *norms, int64_t vstride, int64_t cstride,
@@ -151,6 +222,14 @@ cudaError_t launch_pqr_cluster(double *M, int64_t mstride, int n, double *tau, i
 cudaError_t launch_form_q_rows(const double *V, int64_t vstride, int n, const double *tau,
                                int64_t tstride, double *QT, int64_t qstride, const int *active,
                                int nshift, cudaStream_t st, int kref = 0);
+// multi-cluster versions: nmax = largest n over the jobs (sizes shared memory / grid)
+cudaError_t launch_pqr_cluster_multi(const PqrJob *jobs, int njobs, int nmax, const int *active,
+                                     int nshift, cudaStream_t st);
+cudaError_t launch_form_q_rows_multi(const PqrJob *jobs, int njobs, int nmax, const int *active,
+                                     int nshift, cudaStream_t st);
+cudaError_t launch_tail_rank_multi(const RankJob *jobs, int njobs, int cmax, int nmax,
+                                   const double *tol, const int *active, int nshift,
+                                   cudaStream_t st);
 cudaError_t launch_form_tr(const double *GT, int64_t gstride, int ldg, const double *tau,
                            const int *piv, int64_t vstride, int nR, int t, double *Tr,
                            int64_t tstride, const int *active, int nshift, cudaStream_t st);

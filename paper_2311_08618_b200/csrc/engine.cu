@@ -63,6 +63,7 @@ using Pair = std::pair<int, int>;
 
 
 static inline int64_t pad4(int64_t v) { return (v + 3) / 4 * 4; }
+void launch_pack_counts(const int64_t *counts, const int *status, int64_t *out, int s, cudaStream_t st);
 
 // s-batched device block (row-major, ld = cols)
 struct Blk {
@@ -136,11 +137,14 @@ public:
     void set_option(const std::string &k, int64_t v) {
         if (k == "max_batch") max_batch_ = (int)std::max<int64_t>(1, v);
         else if (k == "time_kernels") time_kernels_ = (int)v;  // 0 off, 1 every kind, 2 Schur only
-        else if (k == "schur_variant") schur_variant_ = (int)v;
         else if (k == "borrow_arena") borrow_arena_ = v != 0;
         else if (k == "elim_order") elim_order_ = (int)v;
         else if (k == "qr_budget") qr_budget_ = v != 0;
         else if (k == "block_cache") block_cache_ = v != 0;
+        else if (k == "schedule") schedule_ = (int)std::max<int64_t>(0, std::min<int64_t>(3, v));
+        else if (k == "window") window_ = (int)std::max<int64_t>(1, v);
+        else if (k == "group_mem_mb") group_mem_mb_ = std::max<int64_t>(1, v);
+        else if (k == "group_max") group_max_ = (int)std::max<int64_t>(1, v);
         else throw CudaFail(H2L_EINVAL, "unknown option " + k);
     }
 
@@ -258,24 +262,6 @@ public:
         uploaded_ = true;
     }
 
-    // ----------------------------------------------------------------- inertia
-    void inertia(const double *mu, int s, int64_t *counts, int32_t *status, h2l_stats *stats) {
-        if (!uploaded_) throw CudaFail(H2L_ESTATE, "h2l_inertia before h2l_upload");
-        CK(cudaSetDevice(dev_));
-        h2l_stats acc{};
-        CK(cudaEventRecord(ev_call_[0], st_));
-        for (int w0 = 0; w0 < s; w0 += max_batch_) {
-            const int ws = std::min(max_batch_, s - w0);
-            run_wave(mu + w0, ws, counts + 3 * (int64_t)w0, status + w0, acc);
-        }
-        CK(cudaEventRecord(ev_call_[1], st_));
-        CK(cudaEventSynchronize(ev_call_[1]));
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, ev_call_[0], ev_call_[1]));
-        acc.ms_total = ms;
-        if (stats) *stats = acc;
-    }
-
     // share the uploaded payload of `o` (read-only; `o` keeps ownership)
     void adopt(const Wave &o) {
         CK(cudaSetDevice(dev_));
@@ -284,17 +270,53 @@ public:
         ranges_ = o.ranges_; boff_ = o.boff_; brank_ = o.brank_; bdim_ = o.bdim_;
         dense_ = o.dense_; lowrank_ = o.lowrank_; deferred_ = o.deferred_; coup_off_ = o.coup_off_;
         arena_ = o.arena_; skel_ = o.skel_; skel_diag_ = o.skel_diag_; skel_off_ = o.skel_off_;
-        max_batch_ = o.max_batch_; time_kernels_ = o.time_kernels_; schur_variant_ = o.schur_variant_; elim_order_ = o.elim_order_; qr_budget_ = o.qr_budget_; block_cache_ = o.block_cache_;
+        max_batch_ = o.max_batch_; time_kernels_ = o.time_kernels_; schedule_ = o.schedule_; window_ = o.window_; group_mem_mb_ = o.group_mem_mb_; group_max_ = o.group_max_; elim_order_ = o.elim_order_; qr_budget_ = o.qr_budget_; block_cache_ = o.block_cache_;
         owns_payload_ = false;
         uploaded_ = o.uploaded_;
     }
     cudaStream_t stream() const { return st_; }
+    // after an exception inside a call: drop every working block and per-wave buffer
+    // (errors are swallowed: a sticky CUDA error leaves nothing to recover)
+    void abort_cleanup() {
+        cudaSetDevice(dev_);
+        cudaStreamSynchronize(st_);
+        cudaGetLastError();
+        auto drop = [&](Blk &b) {
+            if (b.p) cudaFreeAsync(guard_mode() ? b.p - GUARD : b.p, st_);
+            b = Blk{};
+        };
+        for (auto &b : diag_) drop(b);
+        for (auto &kv : offd_) drop(kv.second);
+        for (auto &kv : coup_) drop(kv.second);
+        for (auto &kv : fill_) drop(kv.second);
+        diag_.clear(); offd_.clear(); coup_.clear(); fill_.clear();
+        live_.clear();
+        for (auto &kv : bcache_)
+            for (double *p : kv.second) cudaFreeAsync(p, st_);
+        bcache_.clear();
+        bcache_bytes_ = 0;
+        for (void *p : {(void *)d_mu_, (void *)d_tol_, (void *)d_dropped_, (void *)d_counts_,
+                        (void *)d_status_, (void *)d_rank_})
+            if (p) cudaFreeAsync(p, st_);
+        d_mu_ = d_tol_ = d_dropped_ = nullptr;
+        d_counts_ = nullptr;
+        d_status_ = d_rank_ = nullptr;
+        cudaStreamSynchronize(st_);
+        cudaGetLastError();
+        stage_.off = 0;
+        st_acc_ = nullptr;
+        nc_ = 0;
+        offp_.clear(); fillp_.clear(); pendf_.clear();
+    }
     int max_batch() const { return max_batch_; }
     // run one wave (<= max_batch shifts) and accumulate into acc (stream-ordered, synchronous)
-    void run(const double *mu, int s, int64_t *counts, int32_t *status, h2l_stats &acc) {
+    // dev_out (nullable): device rows [s][4] = (neg, zero, pos, status) instead of the
+    // host counts / status (h2l_inertia_device)
+    void run(const double *mu, int s, int64_t *counts, int32_t *status, h2l_stats &acc,
+             int64_t *dev_out = nullptr) {
         if (!uploaded_) throw CudaFail(H2L_ESTATE, "h2l_inertia before h2l_upload");
         CK(cudaSetDevice(dev_));
-        run_wave(mu, s, counts, status, acc);
+        run_wave(mu, s, counts, status, acc, dev_out);
     }
 
     std::string err;
@@ -307,7 +329,12 @@ private:
     Staging stage_;
     int max_batch_ = 64;
     int time_kernels_ = 0;
-    int schur_variant_ = 0, elim_order_ = 0;
+    int elim_order_ = 0;
+    int schedule_ = 1;                // 0 one cluster per group, 1 ascending wavefronts, 2 colours,
+                                      // 3 colours of consecutive windows of the order
+    int window_ = 64;
+    int64_t group_mem_mb_ = 8192;     // temporaries of one group's eliminations
+    int group_max_ = 512;
     int t_level_max_ = -1;  // largest recompression rank of the current level (-1: none yet)
     bool qr_budget_ = true;
     bool uploaded_ = false;
@@ -337,14 +364,6 @@ private:
     std::vector<Blk> diag_;
     std::vector<int> tile_map_, seg_of_, seg_start_;
     std::vector<SchurTarget> schur_tbl_;
-    static bool bk_single_mode() {
-        static const bool on = getenv("H2L_BK_SINGLE") != nullptr;
-        return on;
-    }
-    static bool schur_pairs_mode() {
-        static const bool on = getenv("H2L_SCHUR_PAIRS") != nullptr;
-        return on;
-    }
     std::vector<char> elim_, pend_diag_;
     std::set<Pair> pend_off_;          // pending dense leaf blocks (large levels)
     // flat pair index of the current level (nc_ <= FLAT_MAX): O(1) block lookups
@@ -379,6 +398,10 @@ private:
     void fill_erase(const Pair &k) {
         fill_.erase(k);
         if (flat()) fillp_[pidx(k)] = nullptr;
+    }
+    bool pend_has(const Pair &k) const {
+        if (flat()) return k.first < nc_ && k.second < nc_ && pendf_[pidx(k)];
+        return pend_off_.count(k) != 0;
     }
     bool pend_test_clear(const Pair &k) {
         if (flat()) {
@@ -422,7 +445,15 @@ private:
         owns_payload_ = true;
     }
 
-    const void *stage(const void *src, size_t nbytes) {
+    // Task lists reach the device through a pinned ring and one H2D copy per
+    // launch.  Every array a launch reads is reserved in ONE region: a ring
+    // overflow (stream sync + reset, or growth) can only happen before the
+    // region is handed out, never between two arrays of the same launch.
+    struct StageRegion {
+        char *h = nullptr, *d = nullptr;
+        size_t n = 0;
+    };
+    StageRegion stage_begin(size_t nbytes) {
         const size_t bytes = (nbytes + 255) / 256 * 256;
         if (stage_.off + bytes > stage_.cap) {
             sync();
@@ -431,13 +462,29 @@ private:
                 stage_.init(bytes * 2);
             }
         }
-        char *h = stage_.h + stage_.off;
-        char *d = stage_.d + stage_.off;
-        std::memcpy(h, src, nbytes);
-        CK(cudaMemcpyAsync(d, h, nbytes, cudaMemcpyHostToDevice, st_));
+        StageRegion r{stage_.h + stage_.off, stage_.d + stage_.off, nbytes};
         stage_.off += bytes;
-        return d;
+        return r;
     }
+    void stage_commit(const StageRegion &r) {
+        if (r.n) CK(cudaMemcpyAsync(r.d, r.h, r.n, cudaMemcpyHostToDevice, st_));
+    }
+    const void *stage(const void *src, size_t nbytes) {
+        StageRegion r = stage_begin(nbytes);
+        std::memcpy(r.h, src, nbytes);
+        stage_commit(r);
+        return r.d;
+    }
+    // several host arrays packed into one staged region (16-byte aligned parts)
+    struct Pack {
+        std::vector<char> h;
+        size_t add(const void *p, size_t n) {
+            const size_t off = (h.size() + 15) / 16 * 16;
+            h.resize(off + n);
+            if (n) std::memcpy(h.data() + off, p, n);
+            return off;
+        }
+    };
     // H2L_GEMMSTATS: flop-weighted histogram of Schur GEMM shapes (printed per wave)
     std::map<std::string, double> ghist_;
     static bool gemmstats_on() {
@@ -622,8 +669,12 @@ private:
     }
     void flush(CopyBatch &b, const double *mu = nullptr) {
         if (!b.t.empty()) {
-            const CopyTask *dt = (const CopyTask *)stage(b.t.data(), sizeof(CopyTask) * b.t.size());
-            const int *dp = (const int *)stage(b.pre.data(), sizeof(int) * b.pre.size());
+            Pack pk;
+            const size_t o1 = pk.add(b.t.data(), sizeof(CopyTask) * b.t.size());
+            const size_t o2 = pk.add(b.pre.data(), sizeof(int) * b.pre.size());
+            const char *d = (const char *)stage(pk.h.data(), pk.h.size());
+            const CopyTask *dt = (const CopyTask *)(d + o1);
+            const int *dp = (const int *)(d + o2);
             {
                 Timed tm(this, 5);
                 launch_copy_prefixed(dt, dp, (int)b.t.size(), b.tiles, s_ ? s_ : 1, mu, st_);
@@ -662,17 +713,23 @@ private:
     // kind: 1 = Schur update, 0 = other
     void flush(GemmBatch &b, int nshift, int kind = 0) {
         if (!b.t.empty()) {
-            const GemmTask *dt = (const GemmTask *)stage(b.t.data(), sizeof(GemmTask) * b.t.size());
-            const int *dp = (const int *)stage(b.pre.data(), sizeof(int) * b.pre.size());
-            const int *dm = nullptr;
-            if (b.t.size() > 32) {  // tile -> task map: one load per CTA instead of a search
+            Pack pk;
+            const size_t o1 = pk.add(b.t.data(), sizeof(GemmTask) * b.t.size());
+            const size_t o2 = pk.add(b.pre.data(), sizeof(int) * b.pre.size());
+            size_t o3 = 0;
+            const bool map = b.t.size() > 32;  // tile -> task map: one load per CTA instead of a search
+            if (map) {
                 tile_map_.resize(b.tiles);
                 for (size_t q = 0; q < b.t.size(); ++q) {
                     const int e = q + 1 < b.t.size() ? b.pre[q + 1] : b.tiles;
                     std::fill(tile_map_.begin() + b.pre[q], tile_map_.begin() + e, (int)q);
                 }
-                dm = (const int *)stage(tile_map_.data(), sizeof(int) * tile_map_.size());
+                o3 = pk.add(tile_map_.data(), sizeof(int) * tile_map_.size());
             }
+            const char *d = (const char *)stage(pk.h.data(), pk.h.size());
+            const GemmTask *dt = (const GemmTask *)(d + o1);
+            const int *dp = (const int *)(d + o2);
+            const int *dm = map ? (const int *)(d + o3) : nullptr;
             {
                 Timed tm(this, kind);
                 launch_gemm(dt, dp, (int)b.t.size(), b.tiles, nshift, st_, kind == 1, dm);
@@ -709,7 +766,8 @@ private:
     Blk &pair_block(std::map<Pair, Blk> &store, int a, int b) { return store[{a, b}]; }
 
     // ------------------------------------------------------------------ wave
-    void run_wave(const double *mu, int s, int64_t *counts, int32_t *status, h2l_stats &acc) {
+    void run_wave(const double *mu, int s, int64_t *counts, int32_t *status, h2l_stats &acc,
+                  int64_t *dev_out) {
         const auto wall0 = std::chrono::steady_clock::now();
         wait_ms_ = host_rec_ms_ = host_elim_ms_ = 0.0;
         s_ = s;
@@ -768,9 +826,14 @@ private:
         // timings of Schur launches
         std::vector<int64_t> hc(3 * s);
         std::vector<int> hs(s);
-        std::vector<double> hd(s);
-        CK(cudaMemcpyAsync(hc.data(), d_counts_, sizeof(int64_t) * 3 * s, cudaMemcpyDeviceToHost, st_));
-        CK(cudaMemcpyAsync(hs.data(), d_status_, sizeof(int) * s, cudaMemcpyDeviceToHost, st_));
+        if (dev_out) {
+            launch_pack_counts(d_counts_, d_status_, dev_out, s, st_);
+            CK(cudaGetLastError());
+            st_acc_->launches++;
+        } else {
+            CK(cudaMemcpyAsync(hc.data(), d_counts_, sizeof(int64_t) * 3 * s, cudaMemcpyDeviceToHost, st_));
+            CK(cudaMemcpyAsync(hs.data(), d_status_, sizeof(int) * s, cudaMemcpyDeviceToHost, st_));
+        }
         sync();
         for (auto &mk : ev_marks_) {
             float ms = 0.f;
@@ -780,12 +843,17 @@ private:
             if (kd == 1) acc.ms_schur += ms;
             if (kd == 3) acc.ms_bk += ms;
         }
-        std::memcpy(counts, hc.data(), sizeof(int64_t) * 3 * s);
-        for (int z = 0; z < s; ++z) status[z] = hs[z] ? H2L_SHIFT_SINGULAR : H2L_SHIFT_OK;
+        if (!dev_out) {
+            std::memcpy(counts, hc.data(), sizeof(int64_t) * 3 * s);
+            for (int z = 0; z < s; ++z) status[z] = hs[z] ? H2L_SHIFT_SINGULAR : H2L_SHIFT_OK;
+        }
         for (double *p : {d_mu_, d_tol_, d_dropped_}) CK(cudaFreeAsync(p, st_));
         CK(cudaFreeAsync(d_counts_, st_));
         CK(cudaFreeAsync(d_status_, st_));
         CK(cudaFreeAsync(d_rank_, st_));
+        d_mu_ = d_tol_ = d_dropped_ = nullptr;
+        d_counts_ = nullptr;
+        d_status_ = d_rank_ = nullptr;
         sync();
         if (hostprof_on())
             fprintf(stderr, "hostprof: wave of %d shifts: wall %.1f ms, blocked in syncs %.1f ms, "
@@ -885,9 +953,8 @@ private:
         off_put(pr, b);
     }
     // every block the recompression and elimination of i can touch
-    void ensure_front(int i) {
+    void ensure_front(int i, CopyBatch &c) {
         if (npend_ == 0 && npend_diag_ == 0) return;
-        CopyBatch c;
         ensure_diag(i, c);
         std::vector<int> partners;
         for (auto &k : adj_off_[i]) {
@@ -901,7 +968,6 @@ private:
                 for (size_t y = x + 1; y < partners.size(); ++y)
                     ensure_off({partners[x], partners[y]}, c);
         }
-        flush(c, d_mu_);
     }
     void ensure_all() {
         CopyBatch c;
@@ -910,31 +976,157 @@ private:
         flush(c, d_mu_);
     }
 
-    void process_level(int level) {
+    // ------------------------------------------------------ elimination schedule
+    // Groups of clusters of one level that are eliminated together (one launch
+    // per kernel kind for the whole group).  Two clusters may share a group
+    // only if their eliminations touch disjoint blocks: with N(i) = {i} and its
+    // near-field partners, eliminating i writes diag/offd/fill blocks inside
+    // N(i) x N(i) and rotates / compacts the fills of i, so i and i' conflict
+    // when N(i) and N(i') intersect or a fill (i, i') exists when the level
+    // starts (fills created during the level join two partners of one cluster,
+    // which already intersect).  Couplings both may pad are composed on the host.
+    //   schedule 0: one cluster per group, ascending (the reference, gldl.py:262-266)
+    //               or low-degree first (elim_order 1);
+    //   schedule 1: wavefronts of the ascending order's dependency DAG -- every
+    //               cluster runs after all earlier conflicting ones, so each
+    //               shift factors exactly what the ascending sweep factors;
+    //   schedule 2: colour classes of a greedy distance-2 colouring (ascending
+    //               first-fit): a re-ordered elimination, far fewer groups.
+    std::vector<std::vector<int>> make_schedule(int level) {
         const int nc = 1 << level;
-        const bool leaf = level == depth_;
-        t_level_max_ = -1;
-        // elimination order: ascending (the reference, gldl.py:263) or, with the
-        // "elim_order" option, low near-field degree first (smaller fronts: the
-        // config-4 sphere does not fit one B200 in ascending order); the inertia
-        // is order-independent, the fill pattern and ranks are not
-        std::vector<int> order(nc);
-        for (int i = 0; i < nc; ++i) order[i] = i;
+        std::vector<int> order;
+        for (int i = 0; i < nc; ++i)
+            if (cl_[i].m > 0) order.push_back(i);
         if (elim_order_ == 1)
             std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
                 return adj_off_[a].size() + adj_fill_[a].size() < adj_off_[b].size() + adj_fill_[b].size();
             });
-        for (int i : order) {
-            if (cl_[i].m == 0) continue;
-            if (leaf) ensure_front(i);
+        std::vector<std::vector<int>> groups;
+        if (schedule_ == 0 || order.size() <= 1) {
+            for (int i : order) groups.push_back({i});
+            return groups;
+        }
+        const int W = (nc + 63) / 64;
+        std::vector<uint64_t> N((size_t)nc * W, 0), F((size_t)nc * W, 0);
+        auto setb = [&](std::vector<uint64_t> &v, int r, int b) { v[(size_t)r * W + (b >> 6)] |= 1ull << (b & 63); };
+        for (int i = 0; i < nc; ++i) {
+            setb(N, i, i);
+            for (auto &k : adj_off_[i]) setb(N, i, k.first == i ? k.second : k.first);
+            for (auto &k : adj_fill_[i]) setb(F, i, k.first == i ? k.second : k.first);
+        }
+        auto inter = [&](const std::vector<uint64_t> &a, int ra, const uint64_t *b) {
+            for (int w = 0; w < W; ++w)
+                if (a[(size_t)ra * W + w] & b[w]) return true;
+            return false;
+        };
+        std::vector<int> gid(nc, -1);
+        if (schedule_ == 1) {
+            // wavefront w(i) = 1 + max w(i') over earlier conflicting i'
+            std::vector<int> om(nc, -1);  // max wavefront of a processed cluster whose N holds x
+            for (int i : order) {
+                int w = 0;
+                for (int x = 0; x < nc; ++x)
+                    if ((N[(size_t)i * W + (x >> 6)] >> (x & 63)) & 1) w = std::max(w, om[x] + 1);
+                for (auto &k : adj_fill_[i]) {
+                    const int f = k.first == i ? k.second : k.first;
+                    if (gid[f] >= 0) w = std::max(w, gid[f] + 1);
+                }
+                gid[i] = w;
+                for (int x = 0; x < nc; ++x)
+                    if ((N[(size_t)i * W + (x >> 6)] >> (x & 63)) & 1) om[x] = std::max(om[x], w);
+            }
+        } else {
+            // first-fit colouring: colour c holds the union of its members' N and its
+            // members.  Schedule 3 colours consecutive windows of the order separately
+            // (groups: window 0's colours, then window 1's, ...): the eliminated clusters
+            // stay a moving front, so materialised blocks and fills stay local as in the
+            // ascending sweep (schedule 2 spreads them over the whole level at once)
+            const int win = schedule_ == 3 ? std::max(1, window_) : (int)order.size();
+            int base = 0;
+            for (size_t w0 = 0; w0 < order.size(); w0 += win) {
+                std::vector<std::vector<uint64_t>> U, Mb;
+                const size_t w1 = std::min(order.size(), w0 + win);
+                for (size_t q = w0; q < w1; ++q) {
+                    const int i = order[q];
+                    int c = 0;
+                    for (; c < (int)U.size(); ++c)
+                        if (!inter(N, i, U[c].data()) && !inter(F, i, Mb[c].data())) break;
+                    if (c == (int)U.size()) {
+                        U.emplace_back(W, 0);
+                        Mb.emplace_back(W, 0);
+                    }
+                    for (int w = 0; w < W; ++w) U[c][w] |= N[(size_t)i * W + w];
+                    Mb[c][i >> 6] |= 1ull << (i & 63);
+                    gid[i] = base + c;
+                }
+                base += (int)U.size();
+            }
+        }
+        int ng = 0;
+        for (int i : order) ng = std::max(ng, gid[i] + 1);
+        std::vector<std::vector<int>> byg(ng);
+        for (int i : order) byg[gid[i]].push_back(i);
+        // split a group by the temporaries its eliminations hold at once
+        const double budget = (double)group_mem_mb_ * 1048576.0;
+        for (auto &g : byg) {
+            std::sort(g.begin(), g.end());
+            std::vector<int> cur;
+            double bytes = 0.0;
+            for (int i : g) {
+                const Cl &ci = cl_[i];
+                double R = ci.nS;
+                for (auto &k : adj_off_[i]) R += cl_[k.first == i ? k.second : k.first].m;
+                int c = 0;
+                for (auto &k : adj_fill_[i]) {
+                    const Blk *f = fill_get(k);
+                    if (f) c += k.first == i ? f->cols : f->rows;
+                }
+                const double m = ci.m;
+                // panel + products, recompression buffers, and the fills the elimination
+                // can create between its partners (upper bound: every partner pair)
+                double fills = 0.0;
+                {
+                    std::vector<int> ps;
+                    for (auto &k : adj_off_[i]) ps.push_back(k.first == i ? k.second : k.first);
+                    for (size_t x = 0; x < ps.size(); ++x)
+                        for (size_t y = x + 1; y < ps.size(); ++y) {
+                            const Pair key{std::min(ps[x], ps[y]), std::max(ps[x], ps[y])};
+                            if (!off_get(key) && !fill_get(key) && !pend_has(key))
+                                fills += (double)cl_[ps[x]].m * cl_[ps[y]].m;
+                        }
+                }
+                const double b = 8.0 * s_ * (2.0 * R * m + 2.0 * (double)c * m + 6.0 * m * m + fills);
+                if (!cur.empty() && (bytes + b > budget || (int)cur.size() >= group_max_)) {
+                    groups.push_back(cur);
+                    cur.clear();
+                    bytes = 0.0;
+                }
+                cur.push_back(i);
+                bytes += b;
+            }
+            if (!cur.empty()) groups.push_back(cur);
+        }
+        return groups;
+    }
+
+    void process_level(int level) {
+        const bool leaf = level == depth_;
+        t_level_max_ = -1;
+        const auto groups = make_schedule(level);
+        st_acc_->groups += (int64_t)groups.size();
+        for (const auto &g : groups) {
+            if (leaf && (npend_ || npend_diag_)) {
+                CopyBatch c;
+                for (int i : g) ensure_front(i, c);
+                flush(c, d_mu_);
+            }
             const auto h0 = std::chrono::steady_clock::now();
-            recompress(i);
+            recompress_group(g);
             const auto h1 = std::chrono::steady_clock::now();
-            eliminate(i);
+            eliminate_group(g);
             const auto h2 = std::chrono::steady_clock::now();
             host_rec_ms_ += std::chrono::duration<double, std::milli>(h1 - h0).count();
             host_elim_ms_ += std::chrono::duration<double, std::milli>(h2 - h1).count();
-            if ((i & (nc / 8 - 1)) == 0 && nc >= 8) memtrace("cluster", i);
         }
         if (leaf) ensure_all();
         // fold fills of this level's low-rank pairs into the couplings (gldl.py:284-294)
@@ -985,9 +1177,8 @@ private:
         add_copy(c, cp(src.at(0, nR), src.bs, m, dst.at(0, newR), dst.bs, m, rows, nS));
     }
 
-    // Q^T of the full column-pivoted QR of the n x n Gram matrix M (M is consumed):
-    // the cluster kernel keeps M in distributed shared memory; beyond its capacity
-    // the single-CTA kernel pair runs on M in global memory
+    // Q^T of the full column-pivoted QR of the n x n Gram matrix M (M is consumed),
+    // one cluster: the deflation pass and the fallback beyond distributed shared memory
     void gram_order(Blk &M, int n, Blk &QT, double *tau, int *piv, int *used, double *norms,
                     int64_t ts, const int *d_active, int kmax) {
         if (pqr_cluster_size(n)) {
@@ -1000,248 +1191,411 @@ private:
             // all n reflectors; with t = n form_tr's row map is the identity (QT = Q^T)
             CK(launch_form_tr(M.p, M.bs, n, tau, piv, ts, n, n, QT.p, QT.bs, d_active, s_, st_));
         }
+        st_acc_->launches += 2;
     }
 
-    // M (n x n) = A^T A for A = c x n (row stride ld, shift stride sA).  The
-    // contraction runs over c (up to ~10^5) with only (n/64)^2 output tiles, so it
-    // is split over K into partial products (one grouped launch) summed in a fixed
-    // order by a second kernel: enough CTAs to fill the SMs
+    // M (n x n) = A^T A for A = c x n (row stride ld, shift stride sA), one cluster
     void gram(const double *A, int64_t sA, int ld, int n, int c, Blk &M) {
-        const int tiles = gemm_tiles(n, n);
-        int parts = std::max(1, std::min((c + 511) / 512, (2 * 148 * 4 + tiles - 1) / std::max(1, tiles)));
-        if (parts <= 1) {
-            GemmBatch g;
-            add_gemm(g, gm(A, sA, ld, 1, A, sA, ld, 0, M.p, M.bs, n, n, n, c, 1.0, 0.0), s_);
-            flush(g, s_, 6);
-            return;
-        }
-        const int chunk = (c + parts - 1) / parts;
-        parts = (c + chunk - 1) / chunk;
-        const int64_t ps = pad4((int64_t)n * n);
-        double *P;
-        CK(cudaMallocFromPoolAsync((void **)&P, sizeof(double) * ps * parts * s_, pool_, st_));
         GemmBatch g;
-        for (int q = 0; q < parts; ++q) {
-            const int k0 = q * chunk, kc = std::min(chunk, c - k0);
-            add_gemm(g, gm(A + (int64_t)k0 * ld, sA, ld, 1, A + (int64_t)k0 * ld, sA, ld, 0,
-                           P + q * ps, ps * parts, n, n, n, kc, 1.0, 0.0), s_);
-        }
+        add_gemm(g, gm(A, sA, ld, 1, A, sA, ld, 0, M.p, M.bs, n, n, n, c, 1.0, 0.0), s_);
         flush(g, s_, 6);
-        {
-            Timed tm(this, 6);
-            launch_sum_partials(P, ps * parts, ps, parts, M.p, M.bs, (int64_t)n * n, s_, st_);
-        }
-        CK(cudaGetLastError());
-        st_acc_->launches++;
-        CK(cudaFreeAsync(P, st_));
     }
 
-    void recompress(int i) {
-        Cl &ci = cl_[i];
-        const int nR = ci.nR;
-        auto &keys = adj_fill_[i];
-        if (nR == 0 || keys.empty()) return;
-        std::vector<Pair> ks(keys.begin(), keys.end());
-        int c = 0;
-        for (auto &k : ks) c += (k.first == i) ? fill_get(k)->cols : fill_get(k)->rows;
-        if (c > 0) {
-            // G^T (c x nR): row q = column q of G
-            Blk GT = alloc(c, nR, false);
+    // one cluster's recompression state (recompress_group)
+    struct RecJob {
+        int i = 0, nR = 0, c = 0, kmax = 0, t = 0;
+        std::vector<Pair> ks;
+        Blk GT, M, QT, DT;
+        double *tau = nullptr, *norms = nullptr, *part = nullptr, *P = nullptr;
+        int *piv = nullptr, *used = nullptr;
+        int parts = 1;
+        double dropped = 0.0;
+    };
+
+    // Recompression of every cluster of a group (gldl.py:296-347), each kernel
+    // kind one launch over all clusters x shifts.  Rank reveal: the reference
+    // runs a column-pivoted QR of the fill rows G (n_R x c); here the directions
+    // are ordered by a pivoted QR of the Gram matrix M = G G^T (cluster kernel)
+    // and the rank is taken from the EXACT energies of D = Q^T G with the
+    // reference's tail rule (k_rrqr.cu).  One readback per group decides the
+    // ranks (block sizes are host-side structure).
+    void recompress_group(const std::vector<int> &grp) {
+        std::vector<RecJob> J;
+        for (int i : grp) {
+            const Cl &ci = cl_[i];
+            if (ci.nR == 0 || adj_fill_[i].empty()) continue;
+            RecJob j;
+            j.i = i;
+            j.nR = ci.nR;
+            j.ks.assign(adj_fill_[i].begin(), adj_fill_[i].end());
+            for (auto &k : j.ks) j.c += (k.first == i) ? fill_get(k)->cols : fill_get(k)->rows;
+            J.push_back(std::move(j));
+        }
+        if (J.empty()) return;
+        const int nj = (int)J.size();
+        // ---- G^T (c x nR) of every job: row q = column q of G
+        {
             CopyBatch cb;
-            int q0 = 0;
-            for (auto &k : ks) {
-                Blk &F = *fill_get(k);
-                if (k.first == i) {  // part = F[:nR, :]  -> GT rows = columns of F
-                    add_copy(cb, cp(F.p, F.bs, F.cols, GT.at(q0, 0), GT.bs, nR, F.cols, nR, 1));
-                    q0 += F.cols;
-                } else {  // part = F[:, :nR]^T -> GT rows = rows of F
-                    add_copy(cb, cp(F.p, F.bs, F.cols, GT.at(q0, 0), GT.bs, nR, F.rows, nR, 0));
-                    q0 += F.rows;
+            for (auto &j : J) {
+                if (j.c == 0) continue;
+                j.GT = alloc(j.c, j.nR, false);
+                int q0 = 0;
+                for (auto &k : j.ks) {
+                    Blk &F = *fill_get(k);
+                    if (k.first == j.i) {  // F[:nR, :] -> GT rows = columns of F
+                        add_copy(cb, cp(F.p, F.bs, F.cols, j.GT.at(q0, 0), j.GT.bs, j.nR, F.cols, j.nR, 1));
+                        q0 += F.cols;
+                    } else {               // F[:, :nR]^T -> GT rows = rows of F
+                        add_copy(cb, cp(F.p, F.bs, F.cols, j.GT.at(q0, 0), j.GT.bs, j.nR, F.rows, j.nR, 0));
+                        q0 += F.rows;
+                    }
                 }
             }
             flush(cb);
-            // ---- rank reveal: order the directions by a column-pivoted QR of the
-            // Gram matrix M = G G^T = U S^2 U^T (its columns are G's columns weighted
-            // toward the dominant singular directions), then take the rank from the
-            // exact energies of D = Q^T G (k_rrqr.cu)
-            Blk M = alloc(nR, nR, false), QT = alloc(nR, nR, false), DT = alloc(c, nR, false);
-            const int64_t ts = pad4(nR);
-            const int64_t pn = tail_rank_part_doubles(c, nR);
-            double *tau, *part, *norms;
-            int *piv, *used, *d_active;
-            CK(cudaMallocFromPoolAsync((void **)&tau, sizeof(double) * ts * s_, pool_, st_));
-            CK(cudaMallocFromPoolAsync((void **)&norms, sizeof(double) * ts * s_, pool_, st_));
-            CK(cudaMallocFromPoolAsync((void **)&piv, sizeof(int) * ts * s_, pool_, st_));
-            CK(cudaMallocFromPoolAsync((void **)&used, sizeof(int) * ts * s_, pool_, st_));
-            CK(cudaMallocFromPoolAsync((void **)&part, sizeof(double) * pn * s_, pool_, st_));
-            CK(cudaMallocFromPoolAsync((void **)&d_active, sizeof(int) * s_, pool_, st_));
-            activity_from_status(d_active);
-            // the ordering is budgeted: kmax pivots (1.5x the largest rank this level
-            // has needed + 32, all of them for the level's first cluster); if the rank
-            // comes within 8 of the budget the ordering is redone with every pivot
-            int kmax = (t_level_max_ < 0 || !qr_budget_)
-                           ? nR : std::min(nR, t_level_max_ + std::max(32, t_level_max_ / 2));
-            int t = 0;
-            double dropped = 0.0;
-            while (true) {
-                gram(GT.p, GT.bs, nR, nR, c, M);  // M = G G^T = GT^T GT
+        }
+        // per-job rank outputs: ranks [nj][s], r1 [nj][s] (ints), dropped [nj][s]
+        int *d_act, *d_ri;
+        double *d_rd;
+        CK(cudaMallocFromPoolAsync((void **)&d_act, sizeof(int) * s_, pool_, st_));
+        CK(cudaMallocFromPoolAsync((void **)&d_ri, sizeof(int) * 2 * nj * s_, pool_, st_));
+        CK(cudaMallocFromPoolAsync((void **)&d_rd, sizeof(double) * nj * s_, pool_, st_));
+        CK(cudaMemsetAsync(d_ri, 0, sizeof(int) * 2 * nj * s_, st_));
+        CK(cudaMemsetAsync(d_rd, 0, sizeof(double) * nj * s_, st_));
+        activity_from_status(d_act);
+        auto rank_of = [&](int q) { return d_ri + (int64_t)q * s_; };
+        auto r1_of = [&](int q) { return d_ri + (int64_t)(nj + q) * s_; };
+        auto drop_of = [&](int q) { return d_rd + (int64_t)q * s_; };
+        for (auto &j : J) {
+            if (j.c == 0) continue;
+            const int64_t ts = pad4(j.nR);
+            j.M = alloc(j.nR, j.nR, false);
+            j.QT = alloc(j.nR, j.nR, false);
+            j.DT = alloc(j.c, j.nR, false);
+            CK(cudaMallocFromPoolAsync((void **)&j.tau, sizeof(double) * ts * s_, pool_, st_));
+            CK(cudaMallocFromPoolAsync((void **)&j.norms, sizeof(double) * ts * s_, pool_, st_));
+            CK(cudaMallocFromPoolAsync((void **)&j.piv, sizeof(int) * ts * s_, pool_, st_));
+            CK(cudaMallocFromPoolAsync((void **)&j.used, sizeof(int) * ts * s_, pool_, st_));
+            CK(cudaMallocFromPoolAsync((void **)&j.part,
+                                       sizeof(double) * tail_rank_part_doubles(j.c, j.nR) * s_, pool_, st_));
+            // the ordering is budgeted: kmax pivots (1.5x the largest rank this level has
+            // needed + 32, all of them for the level's first group); a rank within 8 of the
+            // budget redoes the ordering with every pivot.  The leading kmax reflectors of
+            // a pivoted QR do not depend on how many follow, so the rank equals the full
+            // ordering's; only the (dropped) complement's basis differs.
+            j.kmax = (t_level_max_ < 0 || !qr_budget_)
+                         ? j.nR : std::min(j.nR, t_level_max_ + std::max(32, t_level_max_ / 2));
+        }
+        std::vector<int> pend;
+        for (int q = 0; q < nj; ++q)
+            if (J[q].c > 0) pend.push_back(q);
+        std::vector<int> hri(2 * (size_t)nj * s_), hact(s_);
+        std::vector<double> hrd((size_t)nj * s_);
+        while (!pend.empty()) {
+            // ---- M = G G^T = GT^T GT: split-K partial products (one grouped launch) summed
+            // in a fixed order (one launch), so small groups still fill the SMs
+            {
+                int tiles = 0;
+                for (int q : pend) tiles += gemm_tiles(J[q].nR, J[q].nR);
+                const int want = std::max(1, (2 * 148 * 4 + tiles - 1) / std::max(1, tiles));
+                GemmBatch g;
+                std::vector<SumJob> sj;
+                int64_t maxcount = 0;
+                for (int q : pend) {
+                    RecJob &j = J[q];
+                    const int n = j.nR;
+                    int parts = std::max(1, std::min((j.c + 511) / 512, want));
+                    const int chunk = (j.c + parts - 1) / parts;
+                    parts = (j.c + chunk - 1) / chunk;
+                    j.parts = parts;
+                    if (parts <= 1) {
+                        add_gemm(g, gm(j.GT.p, j.GT.bs, n, 1, j.GT.p, j.GT.bs, n, 0, j.M.p, j.M.bs, n, n, n,
+                                       j.c, 1.0, 0.0), s_);
+                        continue;
+                    }
+                    const int64_t ps = pad4((int64_t)n * n);
+                    if (!j.P) CK(cudaMallocFromPoolAsync((void **)&j.P, sizeof(double) * ps * parts * s_, pool_, st_));
+                    for (int p = 0; p < parts; ++p) {
+                        const int k0 = p * chunk, kc = std::min(chunk, j.c - k0);
+                        add_gemm(g, gm(j.GT.p + (int64_t)k0 * n, j.GT.bs, n, 1, j.GT.p + (int64_t)k0 * n,
+                                       j.GT.bs, n, 0, j.P + p * ps, ps * parts, n, n, n, kc, 1.0, 0.0), s_);
+                    }
+                    sj.push_back(SumJob{j.P, ps * parts, ps, j.M.p, j.M.bs, (int64_t)n * n, parts, 0});
+                    maxcount = std::max<int64_t>(maxcount, (int64_t)n * n);
+                }
+                flush(g, s_, 6);
+                if (!sj.empty()) {
+                    const SumJob *dj = (const SumJob *)stage(sj.data(), sizeof(SumJob) * sj.size());
+                    Timed tm(this, 6);
+                    launch_sum_partials_multi(dj, (int)sj.size(), maxcount, s_, st_);
+                    CK(cudaGetLastError());
+                    st_acc_->launches++;
+                }
+            }
+            // ---- ordering: pivoted QR of every M (cluster kernel) and Q^T
+            {
+                std::vector<PqrJob> pj;
+                int nmax = 0;
+                for (int q : pend) {
+                    RecJob &j = J[q];
+                    if (!pqr_cluster_size(j.nR)) {
+                        st_acc_->paths[3]++;
+                        Timed tm(this, 7);
+                        gram_order(j.M, j.nR, j.QT, j.tau, j.piv, j.used, j.norms, pad4(j.nR), d_act,
+                                   j.kmax);
+                        continue;
+                    }
+                    if (pqr_cluster_size(j.nR) == 16) st_acc_->paths[2]++;
+                    pj.push_back(PqrJob{j.M.p, j.M.bs, j.tau, j.piv, pad4(j.nR), j.QT.p, j.QT.bs, j.nR,
+                                        j.kmax});
+                    nmax = std::max(nmax, j.nR);
+                }
+                if (!pj.empty()) {
+                    const PqrJob *dj = (const PqrJob *)stage(pj.data(), sizeof(PqrJob) * pj.size());
+                    Timed tm(this, 7);
+                    CK(launch_pqr_cluster_multi(dj, (int)pj.size(), nmax, d_act, s_, st_));
+                    CK(launch_form_q_rows_multi(dj, (int)pj.size(), nmax, d_act, s_, st_));
+                    st_acc_->launches += 2;
+                }
+            }
+            // ---- D^T = GT Q (Q[k][n] = QT[n][k]) and the exact tail energies
+            {
+                GemmBatch g;
+                for (int q : pend) {
+                    RecJob &j = J[q];
+                    add_gemm(g, gm(j.GT.p, j.GT.bs, j.nR, 0, j.QT.p, j.QT.bs, j.nR, 1, j.DT.p, j.DT.bs,
+                                   j.nR, j.c, j.nR, j.nR, 1.0, 0.0), s_);
+                }
+                flush(g, s_, 6);
+                std::vector<RankJob> rj;
+                int cmax = 0, nmax = 0;
+                for (int q : pend) {
+                    RecJob &j = J[q];
+                    rj.push_back(RankJob{j.DT.p, j.DT.bs, j.part, rank_of(q), r1_of(q), drop_of(q), j.c, j.nR});
+                    cmax = std::max(cmax, j.c);
+                    nmax = std::max(nmax, j.nR);
+                }
+                const RankJob *dj = (const RankJob *)stage(rj.data(), sizeof(RankJob) * rj.size());
+                Timed tm(this, 6);
+                CK(launch_tail_rank_multi(dj, (int)rj.size(), cmax, nmax, d_tol_, d_act, s_, st_));
+                st_acc_->launches += 2;
+            }
+            auto readback = [&] {
+                CK(cudaMemcpyAsync(hri.data(), d_ri, sizeof(int) * hri.size(), cudaMemcpyDeviceToHost, st_));
+                CK(cudaMemcpyAsync(hrd.data(), d_rd, sizeof(double) * hrd.size(), cudaMemcpyDeviceToHost, st_));
+                CK(cudaMemcpyAsync(hact.data(), d_act, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
+                sync();
+            };
+            readback();
+            // ---- deflation pass: the Gram ordering only resolves directions whose
+            // energy is above ~1e-16 of the largest; re-order the rest from their own
+            // Gram matrix (per cluster; rare).  Skipped when the first pass already drops
+            // every direction past r1: the tail sums from any r <= r1 then include the
+            // whole (rotation-invariant) energy of that subspace.
+            bool defl = false;
+            for (int q : pend) {
+                RecJob &j = J[q];
+                const int nR = j.nR;
+                int r1 = nR, t1 = 0;
+                for (int z = 0; z < s_; ++z)
+                    if (hact[z]) {
+                        r1 = std::min(r1, hri[(size_t)(nj + q) * s_ + z]);
+                        t1 = std::max(t1, hri[(size_t)q * s_ + z]);
+                    }
+                const int nT = nR - r1;
+                if (!(nT > 1 && t1 > r1)) continue;
+                defl = true;
+                Blk M2 = alloc(nT, nT, false), Q2T = alloc(nT, nT, false);
+                Blk DT2 = alloc(j.c, nT, false), QT2 = alloc(nT, nR, false);
+                gram(j.DT.p + r1, j.DT.bs, nR, nT, j.c, M2);  // M2 = D_tail D_tail^T
                 {
                     Timed tm(this, 6);
-                    gram_order(M, nR, QT, tau, piv, used, norms, ts, d_active, kmax);
+                    gram_order(M2, nT, Q2T, j.tau, j.piv, j.used, j.norms, pad4(nR), d_act,
+                               std::min(nT, j.kmax));
                 }
                 {
-                    GemmBatch g;  // D^T = GT Q  (Q[k][n] = QT[n][k])
-                    add_gemm(g, gm(GT.p, GT.bs, nR, 0, QT.p, QT.bs, nR, 1, DT.p, DT.bs, nR, c, nR, nR,
-                                   1.0, 0.0), s_);
+                    GemmBatch g;  // DT2 = D_tail^T Q2 ; QT2 = Q2^T QT[r1:, :]
+                    add_gemm(g, gm(j.DT.p + r1, j.DT.bs, nR, 0, Q2T.p, Q2T.bs, nT, 1, DT2.p, DT2.bs,
+                                   nT, j.c, nT, nT, 1.0, 0.0), s_);
+                    add_gemm(g, gm(Q2T.p, Q2T.bs, nT, 0, j.QT.at(r1, 0), j.QT.bs, nR, 0, QT2.p,
+                                   QT2.bs, nR, nT, nR, nT, 1.0, 0.0), s_);
                     flush(g, s_, 6);
                 }
-                int *d_r1;
-                CK(cudaMallocFromPoolAsync((void **)&d_r1, sizeof(int) * s_, pool_, st_));
+                CopyBatch cc;
+                add_copy(cc, cp(DT2.p, DT2.bs, nT, j.DT.p + r1, j.DT.bs, nR, j.c, nT));
+                add_copy(cc, cp(QT2.p, QT2.bs, nR, j.QT.at(r1, 0), j.QT.bs, nR, nT, nR));
+                flush(cc);
                 {
                     Timed tm(this, 6);
-                    CK(launch_tail_rank(DT.p, DT.bs, c, nR, part, d_tol_, d_rank_, d_dropped_, d_r1,
-                                        d_active, s_, st_));
+                    CK(launch_tail_rank(j.DT.p, j.DT.bs, j.c, nR, j.part, d_tol_, rank_of(q),
+                                        drop_of(q), nullptr, d_act, s_, st_));
+                    st_acc_->launches += 2;
                 }
-                // deflation pass: the Gram matrix only orders directions whose energy is above
-                // ~1e-16 of the largest; re-order the rest from their own Gram matrix
-                {
-                    std::vector<int> r1v(s_), a1(s_), t1v(s_);
-                    CK(cudaMemcpyAsync(r1v.data(), d_r1, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
-                    CK(cudaMemcpyAsync(a1.data(), d_active, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
-                    CK(cudaMemcpyAsync(t1v.data(), d_rank_, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
-                    sync();
-                    int r1 = nR, t1 = 0;
-                    for (int z = 0; z < s_; ++z)
-                        if (a1[z]) {
-                            r1 = std::min(r1, r1v[z]);
-                            t1 = std::max(t1, t1v[z]);
-                        }
-                    const int nT = nR - r1;
-                    // when the first pass already drops every direction past r1 (t1 <= r1)
-                    // re-ordering them cannot change the rank: the tail sums from any
-                    // r <= r1 include the whole (rotation-invariant) energy of that subspace
-                    if (nT > 1 && t1 > r1) {
-                        Blk M2 = alloc(nT, nT, false), Q2T = alloc(nT, nT, false);
-                        Blk DT2 = alloc(c, nT, false), QT2 = alloc(nT, nR, false);
-                        gram(DT.p + r1, DT.bs, nR, nT, c, M2);  // M2 = D_tail D_tail^T
-                        {
-                            Timed tm(this, 6);
-                            gram_order(M2, nT, Q2T, tau, piv, used, norms, ts, d_active, std::min(nT, kmax));
-                        }
-                        {
-                            GemmBatch g;  // DT2 = D_tail^T Q2 ; QT2 = Q2^T QT[r1:, :]
-                            add_gemm(g, gm(DT.p + r1, DT.bs, nR, 0, Q2T.p, Q2T.bs, nT, 1, DT2.p, DT2.bs,
-                                           nT, c, nT, nT, 1.0, 0.0), s_);
-                            add_gemm(g, gm(Q2T.p, Q2T.bs, nT, 0, QT.at(r1, 0), QT.bs, nR, 0, QT2.p,
-                                           QT2.bs, nR, nT, nR, nT, 1.0, 0.0), s_);
-                            flush(g, s_, 6);
-                        }
-                        CopyBatch cc;
-                        add_copy(cc, cp(DT2.p, DT2.bs, nT, DT.p + r1, DT.bs, nR, c, nT));
-                        add_copy(cc, cp(QT2.p, QT2.bs, nR, QT.at(r1, 0), QT.bs, nR, nT, nR));
-                        flush(cc);
-                        {
-                            Timed tm(this, 6);
-                            CK(launch_tail_rank(DT.p, DT.bs, c, nR, part, d_tol_, d_rank_, d_dropped_,
-                                                nullptr, d_active, s_, st_));
-                        }
-                        for (Blk *b : {&M2, &Q2T, &DT2, &QT2}) release(*b);
-                        st_acc_->launches += 8;
-                    }
-                }
-                CK(cudaFreeAsync(d_r1, st_));
-                st_acc_->launches += 5;
-                std::vector<int> rk(s_), act(s_);
-                std::vector<double> dr(s_);
-                CK(cudaMemcpyAsync(rk.data(), d_rank_, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
-                CK(cudaMemcpyAsync(act.data(), d_active, sizeof(int) * s_, cudaMemcpyDeviceToHost, st_));
-                CK(cudaMemcpyAsync(dr.data(), d_dropped_, sizeof(double) * s_, cudaMemcpyDeviceToHost, st_));
-                sync();
-                t = 0;
-                dropped = 0.0;
+                for (Blk *b : {&M2, &Q2T, &DT2, &QT2}) release(*b);
+            }
+            if (defl) readback();
+            std::vector<int> redo;
+            for (int q : pend) {
+                RecJob &j = J[q];
+                j.t = 0;
+                j.dropped = 0.0;
                 for (int z = 0; z < s_; ++z)
-                    if (act[z]) {
-                        t = std::max(t, rk[z]);
-                        dropped += dr[z];
+                    if (hact[z]) {
+                        j.t = std::max(j.t, hri[(size_t)q * s_ + z]);
+                        j.dropped += hrd[(size_t)q * s_ + z];
                     }
-                if (kmax >= nR || t + 8 < kmax) break;
-                kmax = nR;
+                if (j.kmax < j.nR && j.t + 8 >= j.kmax) {
+                    j.kmax = j.nR;
+                    redo.push_back(q);
+                }
             }
-            st_acc_->dropped_fro += dropped;
-            t_level_max_ = std::max(t_level_max_, t);
+            pend.swap(redo);
+        }
+        for (auto &j : J) {
+            if (j.c == 0) continue;
+            st_acc_->dropped_fro += j.dropped;
+            t_level_max_ = std::max(t_level_max_, j.t);
             st_acc_->recompressions++;
-            {   // algorithmic QR of G (nR x c), survey §8d: 2 c nR^2 - 2/3 nR^3 (for c >= nR)
-                const double a = std::max(c, nR), b = std::min(c, nR);
-                st_acc_->flops += (2.0 * a * b * b - 2.0 / 3.0 * b * b * b) * s_;
-            }
-            if (t > 0) {
-                // Tr = [U_r^T ; U_s^T] = QT rows [t, nR) then [0, t)
-                Blk Tr = alloc(nR, nR, false);
-                CopyBatch rc;
-                add_copy(rc, cp(QT.at(t, 0), QT.bs, nR, Tr.p, Tr.bs, nR, nR - t, nR));
-                add_copy(rc, cp(QT.p, QT.bs, nR, Tr.at(nR - t, 0), Tr.bs, nR, t, nR));
-                flush(rc);
-                apply_rotation(i, Tr, t);
-                release(Tr);
-                ci.nR = nR - t;
-                ci.nS += t;
-                st_acc_->rank_added += t;
-            }
-            for (void *q : {(void *)tau, (void *)norms, (void *)piv, (void *)used, (void *)part,
-                            (void *)d_active})
-                CK(cudaFreeAsync(q, st_));
-            for (Blk *b : {&M, &QT, &DT}) release(*b);
-            release(GT);
+            // algorithmic QR of G (nR x c), survey §8d: 2 c nR^2 - 2/3 nR^3 (for c >= nR)
+            const double a = std::max(j.c, j.nR), b = std::min(j.c, j.nR);
+            st_acc_->flops += (2.0 * a * b * b - 2.0 / 3.0 * b * b * b) * s_;
         }
-        // discard what is left in the redundant rows of i's fills (gldl.py:341-347)
-        CopyBatch z;
-        const int keep = ci.nR;
-        for (auto &k : ks) {
-            Blk &F = *fill_get(k);
-            if (keep == 0) continue;
-            if (k.first == i) add_copy(z, zero(F.p, F.bs, F.cols, keep, F.cols));
-            else add_copy(z, zero(F.p, F.bs, F.cols, F.rows, keep));
+        // ---- rotations of every job with t > 0: Tr = [U_r^T ; U_s^T] = QT rows [t, nR) then [0, t)
+        std::vector<int> rot;
+        for (int q = 0; q < nj; ++q)
+            if (J[q].c > 0 && J[q].t > 0) rot.push_back(q);
+        if (!rot.empty()) {
+            std::vector<Blk> Tr(nj);
+            CopyBatch rc;
+            for (int q : rot) {
+                RecJob &j = J[q];
+                Tr[q] = alloc(j.nR, j.nR, false);
+                add_copy(rc, cp(j.QT.at(j.t, 0), j.QT.bs, j.nR, Tr[q].p, Tr[q].bs, j.nR, j.nR - j.t, j.nR));
+                add_copy(rc, cp(j.QT.p, j.QT.bs, j.nR, Tr[q].at(j.nR - j.t, 0), Tr[q].bs, j.nR, j.t, j.nR));
+            }
+            flush(rc);
+            std::vector<int> ids, ts;
+            std::vector<const Blk *> trs;
+            for (int q : rot) {
+                ids.push_back(J[q].i);
+                ts.push_back(J[q].t);
+                trs.push_back(&Tr[q]);
+            }
+            apply_rotations(ids, trs, ts);
+            // per-shift truncation: a shift whose own rank r_z < t drops the fill content
+            // of directions [r_z, t) as the reference does at that shift (gldl.py:341-347);
+            // the directions stay in the skeleton (a congruence: same matrix, same inertia)
+            if (s_ > 1) {
+                std::vector<TailZeroJob> tz;
+                for (int q : rot) {
+                    RecJob &j = J[q];
+                    const Cl &ci = cl_[j.i];  // already rotated: nR' = nR - t, nS' = nS + t
+                    const int base = ci.nR + (ci.nS - j.t);
+                    for (auto &k : adj_fill_[j.i]) {
+                        Blk *F = fill_get(k);
+                        if (!F || !F->p) continue;
+                        if (k.first == j.i)
+                            tz.push_back(TailZeroJob{F->p, F->bs, rank_of(q), F->cols, F->cols, base, j.t, 0, 0});
+                        else
+                            tz.push_back(TailZeroJob{F->p, F->bs, rank_of(q), F->cols, F->rows, base, j.t, 1, 0});
+                    }
+                }
+                if (!tz.empty()) {
+                    const TailZeroJob *dj = (const TailZeroJob *)stage(tz.data(), sizeof(TailZeroJob) * tz.size());
+                    Timed tm(this, 5);
+                    CK(launch_tail_zero(dj, (int)tz.size(), s_, st_));
+                    st_acc_->launches++;
+                }
+            }
+            for (int q : rot) release(Tr[q]);
         }
-        flush(z);
+        // ---- discard what is left in the redundant rows of the fills (gldl.py:341-347)
+        {
+            CopyBatch z;
+            for (auto &j : J) {
+                const int keep = cl_[j.i].nR;
+                if (keep == 0) continue;
+                for (auto &k : j.ks) {
+                    Blk &F = *fill_get(k);
+                    if (k.first == j.i) add_copy(z, zero(F.p, F.bs, F.cols, keep, F.cols));
+                    else add_copy(z, zero(F.p, F.bs, F.cols, F.rows, keep));
+                }
+            }
+            flush(z);
+        }
+        for (auto &j : J) {
+            for (void *p : {(void *)j.tau, (void *)j.norms, (void *)j.piv, (void *)j.used, (void *)j.part,
+                            (void *)j.P})
+                if (p) CK(cudaFreeAsync(p, st_));
+            for (Blk *b : {&j.M, &j.QT, &j.DT, &j.GT}) release(*b);
+        }
+        for (void *p : {(void *)d_act, (void *)d_ri, (void *)d_rd}) CK(cudaFreeAsync(p, st_));
     }
 
     void activity_from_status(int *d_active);
 
-    void apply_rotation(int i, const Blk &Tr, int t) {
-        Cl &ci = cl_[i];
-        const int nR = ci.nR, nS = ci.nS, m = ci.m;
+    // Basis rotations of several clusters (gldl.py:313-339): diag, offd, fill rows /
+    // columns by T, couplings zero-padded.  The clusters of a group share no offd or
+    // fill block; a coupling padded by two of them is padded once to its final size.
+    void apply_rotations(const std::vector<int> &ids, const std::vector<const Blk *> &Trs,
+                         const std::vector<int> &ts) {
         GemmBatch g1, g2;
         CopyBatch c1, c2;
-        // diag: Y = T D ; Z = Y T^T
-        Blk Y = alloc(m, m, false), Z = alloc(m, m, false);
-        row_transform(diag_[i], Y, Tr.p, Tr.bs, nR, nS, t, g1, c1);
+        std::vector<Blk> Y(ids.size()), Z(ids.size());
         std::vector<std::pair<Blk *, Blk>> repl;
-        for (auto *store : {&offd_, &fill_}) {
-            auto &adj = (store == &offd_) ? adj_off_[i] : adj_fill_[i];
-            for (auto &k : adj) {
-                Blk &B = (store == &offd_) ? *off_get(k) : *fill_get(k);
-                Blk N = alloc(B.rows, B.cols, false);
-                if (k.first == i) row_transform(B, N, Tr.p, Tr.bs, nR, nS, t, g1, c1);
-                else col_transform(B, N, Tr.p, Tr.bs, nR, nS, t, g1, c1);
-                repl.push_back({&B, N});
+        for (size_t q = 0; q < ids.size(); ++q) {
+            const int i = ids[q], t = ts[q];
+            const Cl &ci = cl_[i];
+            const Blk &Tr = *Trs[q];
+            Y[q] = alloc(ci.m, ci.m, false);
+            Z[q] = alloc(ci.m, ci.m, false);
+            row_transform(diag_[i], Y[q], Tr.p, Tr.bs, ci.nR, ci.nS, t, g1, c1);  // Y = T D
+            for (auto *store : {&offd_, &fill_}) {
+                auto &adj = (store == &offd_) ? adj_off_[i] : adj_fill_[i];
+                for (auto &k : adj) {
+                    Blk &B = (store == &offd_) ? *off_get(k) : *fill_get(k);
+                    Blk N = alloc(B.rows, B.cols, false);
+                    if (k.first == i) row_transform(B, N, Tr.p, Tr.bs, ci.nR, ci.nS, t, g1, c1);
+                    else col_transform(B, N, Tr.p, Tr.bs, ci.nR, ci.nS, t, g1, c1);
+                    repl.push_back({&B, N});
+                }
             }
         }
         flush(g1, s_, 2);
         flush(c1);
-        col_transform(Y, Z, Tr.p, Tr.bs, nR, nS, t, g2, c2);
-        // couplings: zero-pad by t rows/cols (gldl.py:324-330)
+        for (size_t q = 0; q < ids.size(); ++q) {
+            const int i = ids[q];
+            const Cl &ci = cl_[i];
+            col_transform(Y[q], Z[q], Trs[q]->p, Trs[q]->bs, ci.nR, ci.nS, ts[q], g2, c2);  // Z = Y T^T
+        }
+        // couplings: zero-pad by t rows / columns (gldl.py:324-330)
+        std::map<Pair, std::pair<int, int>> pads;
+        for (size_t q = 0; q < ids.size(); ++q) {
+            const int i = ids[q];
+            for (auto &k : adj_coup_[i]) {
+                auto &pd = pads[k];
+                if (k.first == i) pd.first += ts[q];
+                else pd.second += ts[q];
+            }
+        }
         std::vector<std::pair<Blk *, Blk>> crepl;
-        for (auto &k : adj_coup_[i]) {
-            Blk &C = coup_.at(k);
-            Blk N = (k.first == i) ? alloc(C.rows + t, C.cols, true) : alloc(C.rows, C.cols + t, true);
+        for (auto &kv : pads) {
+            Blk &C = coup_.at(kv.first);
+            Blk N = alloc(C.rows + kv.second.first, C.cols + kv.second.second, true);
             if (C.p && N.p) add_copy(c2, cp(C.p, C.bs, C.cols, N.p, N.bs, N.cols, C.rows, C.cols));
             crepl.push_back({&C, N});
         }
         flush(g2, s_, 2);
         flush(c2);
-        release(diag_[i]);
-        release(Y);
-        diag_[i] = Z;
+        for (size_t q = 0; q < ids.size(); ++q) {
+            const int i = ids[q];
+            release(diag_[i]);
+            release(Y[q]);
+            diag_[i] = Z[q];
+            Cl &ci = cl_[i];
+            ci.nR -= ts[q];
+            ci.nS += ts[q];
+            st_acc_->rank_added += ts[q];
+        }
         for (auto &r : repl) { release(*r.first); *r.first = r.second; }
         for (auto &r : crepl) { release(*r.first); *r.first = r.second; }
     }
@@ -1259,228 +1613,291 @@ private:
         if (g.trans) { *A = g.src + g.r0; *lda = g.lds; *tA = 1; }
         else { *A = g.src + (int64_t)g.r0 * g.lds; *lda = g.lds; *tA = 0; }
     }
-    // op(segment)^T as the right operand (nR x len) of a GEMM
-    static void seg_as_Bt(const Seg &g, const double **B, int *ldb, int *tB) {
-        if (g.trans) { *B = g.src + g.r0; *ldb = g.lds; *tB = 0; }
-        else { *B = g.src + (int64_t)g.r0 * g.lds; *ldb = g.lds; *tB = 1; }
-    }
 
-    void eliminate(int i) {
-        Cl &ci = cl_[i];
-        const int nR = ci.nR, nS = ci.nS, m = ci.m;
-        if (nR == 0) return;
-        st_acc_->max_front = std::max<int64_t>(st_acc_->max_front, m);
-        Blk &D = diag_[i];
-        // ---- K2/K3: BK of D[:nR,:nR] with fused inertia
-        const int64_t ps = pad4(nR);
-        int *perm;
-        double *dinfo;
-        CK(cudaMallocFromPoolAsync((void **)&perm, sizeof(int) * ps * s_, pool_, st_));
-        CK(cudaMallocFromPoolAsync((void **)&dinfo, sizeof(double) * 3 * ps * s_, pool_, st_));
-        bk_launch(D.p, D.bs, m, nR, perm, dinfo, ps);
-        // ---- panel segments (live rows only)
-        std::vector<int> partners;
-        for (auto &k : adj_off_[i]) partners.push_back(k.first == i ? k.second : k.first);
-        std::sort(partners.begin(), partners.end());
+    struct ElimJob {
+        int i = 0, nR = 0, nS = 0, m = 0, R = 0;
         std::vector<Seg> segs;
-        int R = 0;
-        segs.push_back({i, nR, nS, 0, D.at(nR, 0), D.bs, m, 0, 0});
-        R += nS;
-        for (int j : partners) {
-            const int lo = elim_[j] ? cl_[j].nR : 0;
-            Seg g{j, lo, cl_[j].m - lo, R, nullptr, 0, 0, 0, lo};
-            if (i < j) {  // offd(i,j)[:nR, :]^T : panel rows = columns of the block
-                Blk &O = *off_get({i, j});
-                g.src = O.p; g.ss = O.bs; g.lds = O.cols; g.trans = 1;
-            } else {      // offd(j,i)[:, :nR]
-                Blk &O = *off_get({j, i});
-                g.src = O.p; g.ss = O.bs; g.lds = O.cols; g.trans = 0;
-            }
-            segs.push_back(g);
-            R += g.len;
+        int *perm = nullptr;
+        double *dinfo = nullptr;
+        int64_t ps = 0;
+        Blk WI, XI, G, Xb, Bg;
+    };
+
+    // Elimination of every cluster of a group (gldl.py:349-426): BK with fused
+    // inertia, the panel solve on the identity, X = Bg G and the symmetric Schur
+    // update, each one launch over all clusters x shifts; then compaction.
+    void eliminate_group(const std::vector<int> &grp) {
+        std::vector<ElimJob> J;
+        for (int i : grp) {
+            const Cl &ci = cl_[i];
+            if (ci.nR == 0) continue;
+            ElimJob j;
+            j.i = i;
+            j.nR = ci.nR;
+            j.nS = ci.nS;
+            j.m = ci.m;
+            J.push_back(std::move(j));
         }
-        double flops = (double)nR * nR * nR / 3.0;
-        if (R > 0) {
-            // ---- K4/K5 as GEMMs.  The reference forms W = B P^T L^{-T} (dtrsm) and
-            // X = W D^{-1} (dgesv), then updates with X W^T.  Here the panel kernel
-            // solves the n x n identity once: W_I = P^T L^{-T}, X_I = W_I D^{-1}; then
-            // G = X_I W_I^T = P^T L^{-T} D^{-1} L^{-1} P, X = B G on the tensor pipe and
-            // the Schur update is X_a B_b^T (W = B is read in place from its blocks).
-            Blk WI = alloc(nR, nR, false), XI = alloc(nR, nR, false), G = alloc(nR, nR, false);
-            std::vector<PanelTile> tiles;
-            for (int r = 0; r < nR; r += PANEL_ROWS) {
+        if (J.empty()) return;
+        // ---- K2/K3: BK of D[:nR,:nR] with fused inertia (packed triangle in one CTA's
+        // shared memory, or in a thread-block cluster's distributed shared memory)
+        {
+            std::vector<BkJob> small, big;
+            int nsmall = 0, nbig = 0;
+            for (auto &j : J) {
+                st_acc_->max_front = std::max<int64_t>(st_acc_->max_front, j.m);
+                j.ps = pad4(j.nR);
+                CK(cudaMallocFromPoolAsync((void **)&j.perm, sizeof(int) * j.ps * s_, pool_, st_));
+                CK(cudaMallocFromPoolAsync((void **)&j.dinfo, sizeof(double) * 3 * j.ps * s_, pool_, st_));
+                Blk &D = diag_[j.i];
+                const BkJob bj{D.p, D.bs, j.m, j.nR, j.perm, j.dinfo, j.ps};
+                if (bk_scratch_doubles(j.nR) && bk_cluster_size(j.nR)) {
+                    st_acc_->paths[0]++;
+                    big.push_back(bj);
+                    nbig = std::max(nbig, j.nR);
+                } else if (bk_scratch_doubles(j.nR)) {
+                    bk_launch(D.p, D.bs, j.m, j.nR, j.perm, j.dinfo, j.ps);  // beyond the cluster size
+                } else {
+                    small.push_back(bj);
+                    nsmall = std::max(nsmall, j.nR);
+                }
+            }
+            if (!small.empty()) {
+                const BkJob *dj = (const BkJob *)stage(small.data(), sizeof(BkJob) * small.size());
+                Timed tm(this, 3);
+                CK(launch_bk_engine(dj, (int)small.size(), s_, nsmall, d_counts_, d_status_, nullptr, 0, st_));
+                st_acc_->launches++;
+            }
+            if (!big.empty()) {
+                const BkJob *dj = (const BkJob *)stage(big.data(), sizeof(BkJob) * big.size());
+                Timed tm(this, 3);
+                CK(launch_bk_cluster(dj, (int)big.size(), s_, nbig, d_counts_, d_status_, st_));
+                st_acc_->launches++;
+            }
+            dbg_sync("bk");
+        }
+        // ---- panel segments (live rows only)
+        for (auto &j : J) {
+            const int i = j.i;
+            Blk &D = diag_[i];
+            std::vector<int> partners;
+            for (auto &k : adj_off_[i]) partners.push_back(k.first == i ? k.second : k.first);
+            std::sort(partners.begin(), partners.end());
+            j.segs.push_back({i, j.nR, j.nS, 0, D.at(j.nR, 0), D.bs, j.m, 0, 0});
+            j.R = j.nS;
+            for (int p : partners) {
+                const int lo = elim_[p] ? cl_[p].nR : 0;
+                Seg g{p, lo, cl_[p].m - lo, j.R, nullptr, 0, 0, 0, lo};
+                if (i < p) {  // offd(i,p)[:nR, :]^T : panel rows = columns of the block
+                    Blk &O = *off_get({i, p});
+                    g.src = O.p; g.ss = O.bs; g.lds = O.cols; g.trans = 1;
+                } else {      // offd(p,i)[:, :nR]
+                    Blk &O = *off_get({p, i});
+                    g.src = O.p; g.ss = O.bs; g.lds = O.cols; g.trans = 0;
+                }
+                j.segs.push_back(g);
+                j.R += g.len;
+            }
+        }
+        // ---- K4/K5: the panel solve on the nR x nR identity: W_I = P^T L^{-T}, X_I =
+        // W_I D^{-1} (the reference: dtrsm + dgesv on Ball, gldl.py:372-378); then
+        // G = X_I W_I^T = P^T L^{-T} D^{-1} L^{-1} P and X = Bg G on the tensor pipe
+        std::vector<PanelJob> pj;
+        std::vector<PanelTile> tiles;
+        size_t psmem = 0;
+        for (auto &j : J) {
+            if (j.R == 0) continue;
+            Blk &D = diag_[j.i];
+            j.WI = alloc(j.nR, j.nR, false);
+            j.XI = alloc(j.nR, j.nR, false);
+            j.G = alloc(j.nR, j.nR, false);
+            const int jid = (int)pj.size();
+            pj.push_back(PanelJob{D.p, D.bs, j.perm, j.dinfo, j.ps, j.WI.p, j.XI.p, j.WI.bs, j.m, j.nR,
+                                  j.nR, panel_lcw(j.nR)});
+            psmem = std::max(psmem, panel_smem_bytes(j.nR));
+            if (j.nR > 160) st_acc_->paths[1]++;
+            for (int r = 0; r < j.nR; r += PANEL_ROWS) {
                 PanelTile t{};
-                t.src = nullptr; t.row0 = r; t.nrows = std::min(PANEL_ROWS, nR - r); t.src_row0 = r;
+                t.src = nullptr; t.row0 = r; t.nrows = std::min(PANEL_ROWS, j.nR - r); t.src_row0 = r;
+                t.job = jid;
                 tiles.push_back(t);
             }
-            const PanelTile *dt = (const PanelTile *)stage(tiles.data(), sizeof(PanelTile) * tiles.size());
+        }
+        double flops_tot = 0.0, sch_tot = 0.0, bytes_tot = 0.0;
+        for (auto &j : J) flops_tot += (double)j.nR * j.nR * j.nR / 3.0;
+        if (!pj.empty()) {
+            Pack pk;
+            const size_t o1 = pk.add(pj.data(), sizeof(PanelJob) * pj.size());
+            const size_t o2 = pk.add(tiles.data(), sizeof(PanelTile) * tiles.size());
+            const char *d = (const char *)stage(pk.h.data(), pk.h.size());
             {
                 Timed tm(this, 4);
-                CK(launch_panel(dt, (int)tiles.size(), s_, D.p, D.bs, m, nR, perm, dinfo, ps, WI.p,
-                                XI.p, WI.bs, nR, st_));
+                CK(launch_panel_multi((const PanelTile *)(d + o2), (int)tiles.size(), s_,
+                                      (const PanelJob *)(d + o1), psmem, st_));
             }
             dbg_sync("panel");
             st_acc_->launches++;
             GemmBatch g0;
-            add_gemm(g0, gm(XI.p, XI.bs, nR, 0, WI.p, WI.bs, nR, 1, G.p, G.bs, nR, nR, nR, nR, 1.0,
-                            0.0), s_);
+            for (auto &j : J)
+                if (j.R)
+                    add_gemm(g0, gm(j.XI.p, j.XI.bs, j.nR, 0, j.WI.p, j.WI.bs, j.nR, 1, j.G.p, j.G.bs, j.nR,
+                                    j.nR, j.nR, j.nR, 1.0, 0.0), s_);
             flush(g0, s_);
-            Blk Xb = alloc(R, nR, false);
-            CopyBatch fz;  // zeroing of the fill blocks this step creates
-            // target block of a segment pair (x <= y); creates fill blocks (gldl.py:398-409)
-            auto target = [&](size_t x, size_t y, double **C, int64_t *sC, int *ldc, int *trans) {
-                const Seg &a = segs[x], &b = segs[y];
-                *trans = 0;
-                if (x == 0 && y == 0) {
-                    *C = D.at(nR, nR); *sC = D.bs; *ldc = m;
-                } else if (x == y) {
-                    Blk &Dj = diag_[a.who];
-                    *C = Dj.at(a.lo, a.lo); *sC = Dj.bs; *ldc = Dj.cols;
-                } else if (x == 0) {
-                    const int j = b.who;
-                    if (i < j) {
-                        Blk &O = *off_get({i, j});
-                        *C = O.at(nR, b.lo); *sC = O.bs; *ldc = O.cols;
-                    } else {
-                        Blk &O = *off_get({j, i});
-                        *C = O.at(b.lo, nR); *sC = O.bs; *ldc = O.cols; *trans = 1;
-                    }
-                } else {
-                    const Pair key{a.who, b.who};
-                    Blk *T = off_get(key);
-                    if (!T) {
-                        T = fill_get(key);
-                        if (!T) {
-                            // zeroed in one batched launch before the update (fz)
-                            Blk nb = alloc(cl_[a.who].m, cl_[b.who].m, false);
-                            if (nb.p) add_copy(fz, zero(nb.p, nb.bs, nb.cols, nb.rows, nb.cols));
-                            T = fill_put(key, nb);
-                            adj_fill_[a.who].insert(key);
-                            adj_fill_[b.who].insert(key);
-                            st_acc_->fill_blocks++;
-                        }
-                    }
-                    *C = T->at(a.lo, b.lo); *sC = T->bs; *ldc = T->cols;
-                }
-            };
-            double sch = 0.0, sch_bytes = 16.0 * (double)R * nR;  // X and W read once
-            for (size_t x = 0; x < segs.size(); ++x)
-                for (size_t y = x; y < segs.size(); ++y) {
-                    if (segs[x].len <= 0 || segs[y].len <= 0) continue;
-                    sch += (x == y ? 1.0 : 2.0) * (double)segs[x].len * segs[y].len * nR;
-                    sch_bytes += 16.0 * (double)segs[x].len * segs[y].len;  // target r + w
-                }
-            if (!schur_pairs_mode()) {
-                // ---- K5/K6: gather the panel rows Bg = [B_0; B_1; ...] (R x nR), one GEMM
-                // X = Bg G, then the symmetric update C_big -= X Bg^T over the upper
-                // triangle of the R x R panel space, scattered to the target blocks
-                Blk Bg = alloc(R, nR, false);
-                CopyBatch gc;
-                for (auto &sg : segs) {
+            // ---- gather the panel rows Bg = [B_0; B_1; ...] (R x nR) of every job
+            CopyBatch gc;
+            for (auto &j : J) {
+                if (!j.R) continue;
+                j.Bg = alloc(j.R, j.nR, false);
+                j.Xb = alloc(j.R, j.nR, false);
+                for (auto &sg : j.segs) {
                     if (sg.len <= 0) continue;
                     const double *A; int lda, tA;
                     seg_as_A(sg, &A, &lda, &tA);
-                    add_copy(gc, cp(A, sg.ss, lda, Bg.at(sg.row, 0), Bg.bs, nR, sg.len, nR, tA));
+                    add_copy(gc, cp(A, sg.ss, lda, j.Bg.at(sg.row, 0), j.Bg.bs, j.nR, sg.len, j.nR, tA));
                 }
-                flush(gc);
-                GemmBatch g1;
-                add_gemm(g1, gm(Bg.p, Bg.bs, nR, 0, G.p, G.bs, nR, 0, Xb.p, Xb.bs, nR, R, nR, nR,
-                                1.0, 0.0), s_);
-                flush(g1, s_);
+            }
+            flush(gc);
+            GemmBatch g1;
+            for (auto &j : J)
+                if (j.R)
+                    add_gemm(g1, gm(j.Bg.p, j.Bg.bs, j.nR, 0, j.G.p, j.G.bs, j.nR, 0, j.Xb.p, j.Xb.bs,
+                                    j.nR, j.R, j.nR, j.nR, 1.0, 0.0), s_);
+            flush(g1, s_);
+            // ---- K6: C_big -= X Bg^T over the upper triangle of every job's R x R panel
+            // space, scattered to the target blocks (fill blocks created on demand,
+            // zeroed in one batched launch first: gldl.py:398-409)
+            CopyBatch fz;
+            std::vector<SchurJob> sj;
+            std::vector<int> seg_all, start_all, tile_job;
+            std::vector<SchurTarget> tbl_all;
+            std::vector<size_t> seg_off, start_off, tbl_off;
+            int tiles_tot = 0;
+            for (auto &j : J) {
+                if (!j.R) continue;
+                const int i = j.i, nR = j.nR, m = j.m;
+                Blk &D = diag_[i];
+                const auto &segs = j.segs;
                 const int ns = (int)segs.size();
-                seg_of_.assign(R, 0);
-                seg_start_.assign(ns, 0);
-                schur_tbl_.assign((size_t)ns * ns, SchurTarget{nullptr, 0, 0, 0});
+                seg_off.push_back(seg_all.size());
+                start_off.push_back(start_all.size());
+                tbl_off.push_back(tbl_all.size());
                 for (int x = 0; x < ns; ++x) {
-                    seg_start_[x] = segs[x].row;
-                    for (int r = 0; r < segs[x].len; ++r) seg_of_[segs[x].row + r] = x;
+                    start_all.push_back(segs[x].row);
+                    for (int r = 0; r < segs[x].len; ++r) seg_all.push_back(x);
                 }
+                const size_t t0 = tbl_all.size();
+                tbl_all.resize(t0 + (size_t)ns * ns, SchurTarget{nullptr, 0, 0, 0});
+                double sch = 0.0, sch_bytes = 16.0 * (double)j.R * nR;  // X and W read once
                 for (int x = 0; x < ns; ++x)
                     for (int y = x; y < ns; ++y) {
-                        if (segs[x].len <= 0 || segs[y].len <= 0) continue;
-                        SchurTarget &e = schur_tbl_[(size_t)x * ns + y];
-                        target(x, y, &e.base, &e.bs, &e.ldc, &e.trans);
+                        const Seg &a = segs[x], &b = segs[y];
+                        if (a.len <= 0 || b.len <= 0) continue;
+                        sch += (x == y ? 1.0 : 2.0) * (double)a.len * b.len * nR;
+                        sch_bytes += 16.0 * (double)a.len * b.len;  // target r + w
+                        SchurTarget &e = tbl_all[t0 + (size_t)x * ns + y];
+                        e.trans = 0;
+                        if (x == 0 && y == 0) {
+                            e.base = D.at(nR, nR); e.bs = D.bs; e.ldc = m;
+                        } else if (x == y) {
+                            Blk &Dj = diag_[a.who];
+                            e.base = Dj.at(a.lo, a.lo); e.bs = Dj.bs; e.ldc = Dj.cols;
+                        } else if (x == 0) {
+                            const int p = b.who;
+                            if (i < p) {
+                                Blk &O = *off_get({i, p});
+                                e.base = O.at(nR, b.lo); e.bs = O.bs; e.ldc = O.cols;
+                            } else {
+                                Blk &O = *off_get({p, i});
+                                e.base = O.at(b.lo, nR); e.bs = O.bs; e.ldc = O.cols; e.trans = 1;
+                            }
+                        } else {
+                            const Pair key{a.who, b.who};
+                            Blk *T = off_get(key);
+                            if (!T) {
+                                T = fill_get(key);
+                                if (!T) {
+                                    Blk nb = alloc(cl_[a.who].m, cl_[b.who].m, false);
+                                    if (nb.p) add_copy(fz, zero(nb.p, nb.bs, nb.cols, nb.rows, nb.cols));
+                                    T = fill_put(key, nb);
+                                    adj_fill_[a.who].insert(key);
+                                    adj_fill_[b.who].insert(key);
+                                    st_acc_->fill_blocks++;
+                                }
+                            }
+                            e.base = T->at(a.lo, b.lo); e.bs = T->bs; e.ldc = T->cols;
+                        }
                     }
-                flush(fz);
-                const int *d_seg = (const int *)stage(seg_of_.data(), sizeof(int) * R);
-                const int *d_start = (const int *)stage(seg_start_.data(), sizeof(int) * ns);
-                const SchurTarget *d_tbl = (const SchurTarget *)stage(
-                    schur_tbl_.data(), sizeof(SchurTarget) * schur_tbl_.size());
-                {
-                    Timed tm(this, 1);
-                    launch_schur_sym(Xb.p, Bg.p, Xb.bs, nR, R, nR, d_seg, d_start, ns, d_tbl, s_,
-                                     st_, schur_variant_);
-                }
-                CK(cudaGetLastError());
-                dbg_sync("schur-sym");
-                st_acc_->launches++;
-                st_acc_->gemm_flops_exec += 2.0 * (double)schur_sym_tiles(R) * 64 * 64 * nR * s_;
-                release(Bg);
+                const int tl = schur_sym_tiles(j.R);
+                sj.push_back(SchurJob{j.Xb.p, j.Bg.p, j.Xb.bs, nR, j.R, nR, ns, nullptr, nullptr, nullptr,
+                                      tiles_tot, 0});
+                tile_job.insert(tile_job.end(), tl, (int)sj.size() - 1);
+                tiles_tot += tl;
                 // algorithmic panel work (survey §8d): TRSM R nR^2 + D-scale R nR
-                flops += (double)R * nR * nR + (double)R * nR;
-            } else {
-            GemmBatch g1;
-            for (auto &sg : segs) {
-                if (sg.len <= 0) continue;
-                const double *A; int lda, tA;
-                seg_as_A(sg, &A, &lda, &tA);
-                add_gemm(g1, gm(A, sg.ss, lda, tA, G.p, G.bs, nR, 0, Xb.at(sg.row, 0), Xb.bs, nR,
-                                sg.len, nR, nR, 1.0, 0.0), s_);
+                flops_tot += (double)j.R * nR * nR + (double)j.R * nR + sch;
+                sch_tot += sch;
+                bytes_tot += sch_bytes;
+                st_acc_->gemm_flops_exec += 2.0 * (double)tl * 64 * 64 * nR * s_;
             }
-            flush(g1, s_);
-            // algorithmic panel work (survey §8d): TRSM R nR^2 + D-scale R nR
-            flops += (double)R * nR * nR + (double)R * nR;
-            // ---- K6 (H2L_SCHUR_PAIRS=1): one grouped launch of per-pair GEMM tasks
-            GemmBatch g;
-            for (size_t x = 0; x < segs.size(); ++x)
-                for (size_t y = x; y < segs.size(); ++y) {
-                    const Seg &a = segs[x], &b = segs[y];
-                    if (a.len <= 0 || b.len <= 0) continue;
-                    double *C; int64_t sC; int ldc, trans;
-                    target(x, y, &C, &sC, &ldc, &trans);
-                    const Seg &ra = trans ? b : a, &cb = trans ? a : b;
-                    const double *B; int ldb, tB;
-                    seg_as_Bt(cb, &B, &ldb, &tB);
-                    add_gemm(g, gm(Xb.at(ra.row, 0), Xb.bs, nR, 0, B, cb.ss, ldb, tB, C, sC, ldc,
-                                   ra.len, cb.len, nR, -1.0, 1.0), s_);
-                }
             flush(fz);
-            flush(g, s_, 1);
+            // one staged region: segment maps, target tables, tile->job map, job table
+            // (whose pointers into the same region are patched on the host first)
+            Pack pk2;
+            const size_t os = pk2.add(seg_all.data(), sizeof(int) * seg_all.size());
+            const size_t ost = pk2.add(start_all.data(), sizeof(int) * start_all.size());
+            const size_t otb = pk2.add(tbl_all.data(), sizeof(SchurTarget) * tbl_all.size());
+            const size_t otj = pk2.add(tile_job.data(), sizeof(int) * tile_job.size());
+            const size_t osj = pk2.add(sj.data(), sizeof(SchurJob) * sj.size());
+            StageRegion rg = stage_begin(pk2.h.size());
+            SchurJob *hj = (SchurJob *)(pk2.h.data() + osj);
+            for (size_t q = 0; q < sj.size(); ++q) {
+                hj[q].seg_of = (const int *)(rg.d + os) + seg_off[q];
+                hj[q].seg_start = (const int *)(rg.d + ost) + start_off[q];
+                hj[q].tbl = (const SchurTarget *)(rg.d + otb) + tbl_off[q];
             }
-            flops += sch;
-            st_acc_->schur_flops += sch * s_;
-            st_acc_->bytes += sch_bytes * s_;
-            release(WI);
-            release(XI);
-            release(G);
-            release(Xb);
+            std::memcpy(rg.h, pk2.h.data(), pk2.h.size());
+            stage_commit(rg);
+            char *d2 = rg.d;
+            {
+                Timed tm(this, 1);
+                launch_schur_sym_multi((const SchurJob *)(d2 + osj), (const int *)(d2 + otj), tiles_tot,
+                                       s_, st_);
+            }
+            CK(cudaGetLastError());
+            dbg_sync("schur-sym");
+            st_acc_->launches++;
         }
-        st_acc_->flops += flops * s_;
-        st_acc_->elim_flops += flops * s_;
-        // ---- retire the redundant rows / columns of i (gldl.py:411-417).  The
-        // reference zeroes them; here every block of i is compacted to its skeleton
-        // rows / columns (the R part is zero from now on and never read again), and i
+        st_acc_->schur_flops += sch_tot * s_;
+        st_acc_->bytes += bytes_tot * s_;
+        st_acc_->flops += flops_tot * s_;
+        st_acc_->elim_flops += flops_tot * s_;
+        // ---- retire the redundant rows / columns (gldl.py:411-417).  The reference
+        // zeroes them; here every block of i is compacted to its skeleton rows /
+        // columns (the R part is zero from now on and never read again), and i
         // becomes an m = nS, nR = 0 cluster: later panels, Schur targets, merges and
         // fill blocks see only live rows, and the front's memory shrinks as it moves.
         {
             CopyBatch zc;
             std::vector<std::pair<Blk *, Blk>> repl;
-            Blk nd = alloc(nS, nS, false);
-            add_copy(zc, cp(D.at(nR, nR), D.bs, m, nd.p, nd.bs, nS, nS, nS));
-            repl.push_back({&D, nd});
-            for (auto *store : {&offd_, &fill_}) {
-                auto &adj = (store == &offd_) ? adj_off_[i] : adj_fill_[i];
-                for (auto &k : adj) {
-                    Blk &O = (store == &offd_) ? *off_get(k) : *fill_get(k);
-                    Blk N;
-                    if (k.first == i) {
-                        N = alloc(nS, O.cols, false);
-                        add_copy(zc, cp(O.at(nR, 0), O.bs, O.cols, N.p, N.bs, N.cols, nS, O.cols));
-                    } else {
-                        N = alloc(O.rows, nS, false);
-                        add_copy(zc, cp(O.at(0, nR), O.bs, O.cols, N.p, N.bs, N.cols, O.rows, nS));
+            for (auto &j : J) {
+                const int i = j.i, nR = j.nR, nS = j.nS, m = j.m;
+                Blk &D = diag_[i];
+                Blk nd = alloc(nS, nS, false);
+                add_copy(zc, cp(D.at(nR, nR), D.bs, m, nd.p, nd.bs, nS, nS, nS));
+                repl.push_back({&D, nd});
+                for (auto *store : {&offd_, &fill_}) {
+                    auto &adj = (store == &offd_) ? adj_off_[i] : adj_fill_[i];
+                    for (auto &k : adj) {
+                        Blk &O = (store == &offd_) ? *off_get(k) : *fill_get(k);
+                        Blk N;
+                        if (k.first == i) {
+                            N = alloc(nS, O.cols, false);
+                            add_copy(zc, cp(O.at(nR, 0), O.bs, O.cols, N.p, N.bs, N.cols, nS, O.cols));
+                        } else {
+                            N = alloc(O.rows, nS, false);
+                            add_copy(zc, cp(O.at(0, nR), O.bs, O.cols, N.p, N.bs, N.cols, O.rows, nS));
+                        }
+                        repl.push_back({&O, N});
                     }
-                    repl.push_back({&O, N});
                 }
             }
             flush(zc);
@@ -1488,12 +1905,16 @@ private:
                 release(*r.first);
                 *r.first = r.second;
             }
-            ci.m = nS;
-            ci.nR = 0;
         }
-        CK(cudaFreeAsync(perm, st_));
-        CK(cudaFreeAsync(dinfo, st_));
-        elim_[i] = 1;
+        for (auto &j : J) {
+            Cl &ci = cl_[j.i];
+            ci.m = j.nS;
+            ci.nR = 0;
+            elim_[j.i] = 1;
+            for (Blk *b : {&j.WI, &j.XI, &j.G, &j.Xb, &j.Bg}) release(*b);
+            CK(cudaFreeAsync(j.perm, st_));
+            CK(cudaFreeAsync(j.dinfo, st_));
+        }
     }
 
     void bk_launch(double *a, int64_t astride, int ld, int n, int *perm, double *dinfo, int64_t ps) {
@@ -1501,7 +1922,7 @@ private:
         const BkJob *dj = (const BkJob *)stage(&jb, sizeof(jb));
         // fronts beyond one CTA's shared memory: the cluster kernel keeps the packed
         // triangle in distributed shared memory (same arithmetic, bit-identical)
-        if (bk_scratch_doubles(n) && bk_cluster_size(n) && !bk_single_mode()) {
+        if (bk_scratch_doubles(n) && bk_cluster_size(n)) {
             {
                 Timed tm(this, 3);
                 CK(launch_bk_cluster(dj, 1, s_, n, d_counts_, d_status_, st_));
@@ -1755,6 +2176,17 @@ __global__ void active_kernel(const int *status, int *active, int s) {
     int z = blockIdx.x * blockDim.x + threadIdx.x;
     if (z < s) active[z] = status[z] == 0;
 }
+__global__ void pack_counts_kernel(const int64_t *counts, const int *status, int64_t *out, int s) {
+    int z = blockIdx.x * blockDim.x + threadIdx.x;
+    if (z >= s) return;
+    out[4 * z + 0] = counts[3 * z + 0];
+    out[4 * z + 1] = counts[3 * z + 1];
+    out[4 * z + 2] = counts[3 * z + 2];
+    out[4 * z + 3] = status[z] ? H2L_SHIFT_SINGULAR : H2L_SHIFT_OK;
+}
+void launch_pack_counts(const int64_t *counts, const int *status, int64_t *out, int s, cudaStream_t st) {
+    pack_counts_kernel<<<(s + 127) / 128, 128, 0, st>>>(counts, status, out, s);
+}
 void Wave::activity_from_status(int *d_active) {
     active_kernel<<<(s_ + 127) / 128, 128, 0, st_>>>(d_status_, d_active, s_);
     CK(cudaGetLastError());
@@ -1780,6 +2212,8 @@ static void merge_stats(h2l_stats &a, const h2l_stats &b) {
     a.ms_schur += b.ms_schur;
     a.ms_bk += b.ms_bk;
     a.launches += b.launches;
+    a.groups += b.groups;
+    for (int k = 0; k < 4; ++k) a.paths[k] += b.paths[k];
     a.schur_flops += b.schur_flops;
     a.gemm_flops_exec += b.gemm_flops_exec;
     for (int k = 0; k < 8; ++k) a.ms_kind[k] += b.ms_kind[k];
@@ -1810,8 +2244,20 @@ public:
         waves_[0]->upload(pl);
         for (size_t k = 1; k < waves_.size(); ++k) waves_[k]->adopt(*waves_[0]);
     }
-    void inertia(const double *mu, int s, int64_t *counts, int32_t *status, h2l_stats *stats) {
+    void inertia(const double *mu, int s, int64_t *counts, int32_t *status, h2l_stats *stats,
+                 int64_t *dev_out = nullptr) {
         CK(cudaSetDevice(dev_));
+        try {
+            inertia_impl(mu, s, counts, status, stats, dev_out);
+        } catch (...) {
+            // a failed call (device OOM, launch error) must not leave the waves' working
+            // blocks, per-wave buffers or staged task lists behind for the next call
+            for (auto &w : waves_) w->abort_cleanup();
+            throw;
+        }
+    }
+    void inertia_impl(const double *mu, int s, int64_t *counts, int32_t *status, h2l_stats *stats,
+                      int64_t *dev_out) {
         const auto host0 = std::chrono::steady_clock::now();
         const int mb = waves_[0]->max_batch();
         const int nw = (s + mb - 1) / mb;
@@ -1829,7 +2275,9 @@ public:
         auto work = [&](int t) {
             for (int w = t; w < nw; w += C) {
                 const int w0 = w * mb, ws = std::min(mb, s - w0);
-                waves_[t]->run(mu + w0, ws, counts + 3 * (int64_t)w0, status + w0, acc[t]);
+                waves_[t]->run(mu + w0, ws, counts ? counts + 3 * (int64_t)w0 : nullptr,
+                               status ? status + w0 : nullptr, acc[t],
+                               dev_out ? dev_out + 4 * (int64_t)w0 : nullptr);
             }
         };
         if (C == 1) {
@@ -1873,6 +2321,8 @@ public:
         tot.ms_host = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host0).count();
         if (stats) *stats = tot;
     }
+
+    int device() const { return dev_; }
 
 private:
     int dev_;
@@ -1963,6 +2413,13 @@ int h2l_inertia(h2l_engine *engine, const double *mu, int32_t s, int64_t *counts
     return guarded(engine, [&] { engine->impl->inertia(mu, s, counts, status, stats); });
 }
 
+int h2l_inertia_device(h2l_engine *engine, const double *mu, int32_t s, int64_t *dev_counts,
+                       h2l_stats *stats) {
+    if (!engine || s < 0 || (s > 0 && (!mu || !dev_counts))) return H2L_EINVAL;
+    if (s == 0) return H2L_OK;
+    return guarded(engine, [&] { engine->impl->inertia(mu, s, nullptr, nullptr, stats, dev_counts); });
+}
+
 int h2l_set_option(h2l_engine *engine, const char *key, int64_t value) {
     if (!engine || !key) return H2L_EINVAL;
     return guarded(engine, [&] { engine->impl->set_option(key, value); });
@@ -2027,7 +2484,215 @@ int h2l_bk_inertia(int device, const double *a, int64_t n, int32_t count, const 
     });
 }
 
-const char *h2l_version(void) { return "h2ldl 0.1 sm_100a"; }
+const char *h2l_version(void) { return "h2ldl 0.2 sm_100a"; }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- multi-GPU
+// One process, one engine per GPU (each holding a replica of H), shifts sharded
+// in contiguous slices (the reference's chunk rule, parallel.py:85-96), the only
+// exchange an NCCL all-gather of the packed integer counts between the engines'
+// device buffers.  NCCL is opened at h2l_comm_init (dlopen: the library itself
+// does not depend on it, and a process that already loaded NCCL -- e.g. torch's
+// -- reuses that copy).
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace {
+struct NcclApi {
+    void *lib = nullptr;
+    ncclResult_t (*commInitAll)(ncclComm_t *, int, const int *) = nullptr;
+    ncclResult_t (*allGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char *(*errStr)(ncclResult_t) = nullptr;
+    bool load(std::string &err) {
+        if (lib) return true;
+        lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) { err = "libnccl.so.2 not found"; return false; }
+        commInitAll = (decltype(commInitAll))dlsym(lib, "ncclCommInitAll");
+        allGather = (decltype(allGather))dlsym(lib, "ncclAllGather");
+        groupStart = (decltype(groupStart))dlsym(lib, "ncclGroupStart");
+        groupEnd = (decltype(groupEnd))dlsym(lib, "ncclGroupEnd");
+        commDestroy = (decltype(commDestroy))dlsym(lib, "ncclCommDestroy");
+        errStr = (decltype(errStr))dlsym(lib, "ncclGetErrorString");
+        if (!commInitAll || !allGather || !groupStart || !groupEnd || !commDestroy || !errStr) {
+            err = "libnccl.so.2 lacks a required symbol";
+            lib = nullptr;
+            return false;
+        }
+        return true;
+    }
+};
+NcclApi g_nccl;
+std::mutex g_nccl_mu;
+}  // namespace
+
+struct h2l_comm {
+    std::vector<h2l_engine *> eng;
+    std::vector<int> dev;
+    std::vector<ncclComm_t> comm;
+    std::vector<cudaStream_t> st;
+    std::string err;
+};
+
+#define NCK(x)                                                                                   \
+    do {                                                                                         \
+        ncclResult_t r_ = (x);                                                                   \
+        if (r_ != ncclSuccess)                                                                   \
+            throw h2l::CudaFail(H2L_ECUDA, std::string(#x) + ": " + g_nccl.errStr(r_));          \
+    } while (0)
+
+extern "C" {
+
+int h2l_comm_init(h2l_engine *const *engines, int ngpu, h2l_comm **comm) {
+    if (!engines || ngpu <= 0 || !comm) return H2L_EINVAL;
+    *comm = nullptr;
+    for (int r = 0; r < ngpu; ++r)
+        if (!engines[r]) return H2L_EINVAL;
+    return guarded(nullptr, [&] {
+        {
+            std::lock_guard<std::mutex> g(g_nccl_mu);
+            std::string e;
+            if (!g_nccl.load(e)) throw h2l::CudaFail(H2L_ENODEV, e);
+        }
+        auto *c = new h2l_comm;
+        try {
+            for (int r = 0; r < ngpu; ++r) {
+                c->eng.push_back(engines[r]);
+                c->dev.push_back(engines[r]->impl->device());
+            }
+            for (int a = 0; a < ngpu; ++a)
+                for (int b = a + 1; b < ngpu; ++b)
+                    if (c->dev[a] == c->dev[b])
+                        throw h2l::CudaFail(H2L_EINVAL, "h2l_comm_init: two engines on one device");
+            c->comm.assign(ngpu, nullptr);
+            NCK(g_nccl.commInitAll(c->comm.data(), ngpu, c->dev.data()));
+            for (int r = 0; r < ngpu; ++r) {
+                cudaStream_t s;
+                CK(cudaSetDevice(c->dev[r]));
+                CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+                c->st.push_back(s);
+            }
+        } catch (...) {
+            for (auto x : c->comm)
+                if (x) g_nccl.commDestroy(x);
+            delete c;
+            throw;
+        }
+        *comm = c;
+    });
+}
+
+int h2l_comm_destroy(h2l_comm *comm) {
+    if (!comm) return H2L_OK;
+    for (size_t r = 0; r < comm->comm.size(); ++r) {
+        cudaSetDevice(comm->dev[r]);
+        if (r < comm->st.size()) cudaStreamDestroy(comm->st[r]);
+        if (comm->comm[r]) g_nccl.commDestroy(comm->comm[r]);
+    }
+    delete comm;
+    return H2L_OK;
+}
+
+int h2l_inertia_multi(h2l_comm *comm, const double *mu, int32_t s_total, int64_t *counts,
+                      int32_t *status, h2l_stats *stats) {
+    if (!comm || s_total < 0 || (s_total > 0 && (!mu || !counts || !status))) return H2L_EINVAL;
+    if (s_total == 0) return H2L_OK;
+    return guarded(nullptr, [&] {
+        const int G = (int)comm->eng.size();
+        std::vector<int> lo(G), hi(G);
+        const int base = s_total / G, extra = s_total % G;
+        for (int r = 0, p = 0; r < G; ++r) {
+            lo[r] = p;
+            p += base + (r < extra ? 1 : 0);
+            hi[r] = p;
+        }
+        const int width = base + (extra ? 1 : 0);
+        const size_t rowb = sizeof(int64_t) * 4;
+        std::vector<int64_t *> send(G, nullptr), recv(G, nullptr);
+        std::vector<h2l_stats> st(G);
+        std::vector<int> codes(G, 0);
+        std::vector<std::string> errs(G);
+        try {
+            for (int r = 0; r < G; ++r) {
+                CK(cudaSetDevice(comm->dev[r]));
+                CK(cudaMalloc(&send[r], rowb * std::max(1, width)));
+                CK(cudaMalloc(&recv[r], rowb * std::max(1, width) * G));
+                CK(cudaMemset(send[r], 0xff, rowb * std::max(1, width)));  // padding rows: -1
+            }
+            // every engine factorizes its slice on its own host thread (engines are
+            // independent; calls on one engine are never concurrent)
+            std::vector<std::thread> th;
+            for (int r = 0; r < G; ++r)
+                th.emplace_back([&, r] {
+                    try {
+                        cudaSetDevice(comm->dev[r]);
+                        st[r] = h2l_stats{};
+                        if (hi[r] > lo[r])
+                            comm->eng[r]->impl->inertia(mu + lo[r], hi[r] - lo[r], nullptr, nullptr, &st[r],
+                                                        send[r]);
+                    } catch (const h2l::CudaFail &x) {
+                        codes[r] = x.code;
+                        errs[r] = x.what();
+                    } catch (const std::exception &x) {
+                        codes[r] = H2L_EINVAL;
+                        errs[r] = x.what();
+                    }
+                });
+            for (auto &t : th) t.join();
+            for (int r = 0; r < G; ++r)
+                if (codes[r]) throw h2l::CudaFail(codes[r], "rank " + std::to_string(r) + ": " + errs[r]);
+            NCK(g_nccl.groupStart());
+            for (int r = 0; r < G; ++r) {
+                CK(cudaSetDevice(comm->dev[r]));
+                NCK(g_nccl.allGather(send[r], recv[r], (size_t)4 * width, ncclInt64, comm->comm[r],
+                                     comm->st[r]));
+            }
+            NCK(g_nccl.groupEnd());
+            for (int r = 0; r < G; ++r) {
+                CK(cudaSetDevice(comm->dev[r]));
+                CK(cudaStreamSynchronize(comm->st[r]));
+            }
+            std::vector<int64_t> h((size_t)4 * width * G);
+            CK(cudaSetDevice(comm->dev[0]));
+            CK(cudaMemcpy(h.data(), recv[0], h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost));
+            for (int r = 0; r < G; ++r)
+                for (int q = lo[r]; q < hi[r]; ++q) {
+                    const int64_t *row = h.data() + ((size_t)r * width + (q - lo[r])) * 4;
+                    counts[3 * (int64_t)q] = row[0];
+                    counts[3 * (int64_t)q + 1] = row[1];
+                    counts[3 * (int64_t)q + 2] = row[2];
+                    status[q] = (int32_t)row[3];
+                }
+            if (stats) {
+                h2l_stats tot{};
+                for (int r = 0; r < G; ++r) {
+                    h2l::merge_stats(tot, st[r]);
+                    tot.ms_total = std::max(tot.ms_total, st[r].ms_total);  // max over ranks
+                    tot.ms_host = std::max(tot.ms_host, st[r].ms_host);
+                    tot.mem_peak = std::max(tot.mem_peak, st[r].mem_peak);
+                }
+                *stats = tot;
+            }
+        } catch (...) {
+            for (int r = 0; r < G; ++r) {
+                cudaSetDevice(comm->dev[r]);
+                if (send[r]) cudaFree(send[r]);
+                if (recv[r]) cudaFree(recv[r]);
+            }
+            throw;
+        }
+        for (int r = 0; r < G; ++r) {
+            cudaSetDevice(comm->dev[r]);
+            cudaFree(send[r]);
+            cudaFree(recv[r]);
+        }
+    });
+}
 
 }  // extern "C"
 

@@ -109,3 +109,55 @@ void launch_sum_partials(const double *in, int64_t zin, int64_t pstride, int npa
                                                                count);
 }
 }  // namespace h2l
+
+namespace h2l {
+namespace {
+// split-K partial sums of several clusters' Gram products (blockIdx.z = job)
+__global__ void __launch_bounds__(256) sum_partials_multi_kernel(const SumJob *jobs) {
+    const SumJob jb = jobs[blockIdx.z];
+    const int z = blockIdx.y;
+    const double *src = jb.in + z * jb.zin;
+    double *dst = jb.out + z * jb.zout;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < jb.count;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int s = 0; s < jb.nparts; ++s) acc += src[s * jb.pstride + e];
+        dst[e] = acc;
+    }
+}
+
+// per-shift truncation (gldl.py:296-347 with each shift's own rank): zero the
+// rows / columns [base + rank[z], base + t) of a block for shift z
+__global__ void __launch_bounds__(256) tail_zero_kernel(const TailZeroJob *jobs) {
+    const TailZeroJob jb = jobs[blockIdx.x];
+    const int z = blockIdx.y;
+    const int lo = jb.base + min(jb.rank[z], jb.t), hi = jb.base + jb.t;
+    if (hi <= lo) return;
+    double *p = jb.p + z * jb.bs;
+    const int span = hi - lo;
+    const int64_t tot = (int64_t)span * jb.other;
+    for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
+        if (jb.orient == 0) {  // rows lo..hi-1, all `other` columns
+            const int r = lo + (int)(e / jb.other), c = (int)(e % jb.other);
+            p[(int64_t)r * jb.ld + c] = 0.0;
+        } else {               // columns lo..hi-1 of all `other` rows
+            const int r = (int)(e / span), c = lo + (int)(e % span);
+            p[(int64_t)r * jb.ld + c] = 0.0;
+        }
+    }
+}
+}  // namespace
+
+void launch_sum_partials_multi(const SumJob *jobs, int njobs, int64_t max_count, int nshift,
+                               cudaStream_t st) {
+    if (njobs <= 0 || max_count <= 0 || nshift <= 0) return;
+    const int blocks = (int)std::min<int64_t>(256, (max_count + 255) / 256);
+    sum_partials_multi_kernel<<<dim3(blocks, nshift, njobs), 256, 0, st>>>(jobs);
+}
+
+cudaError_t launch_tail_zero(const TailZeroJob *jobs, int njobs, int nshift, cudaStream_t st) {
+    if (njobs <= 0 || nshift <= 0) return cudaSuccess;
+    tail_zero_kernel<<<dim3(njobs, nshift), 256, 0, st>>>(jobs);
+    return cudaGetLastError();
+}
+}  // namespace h2l

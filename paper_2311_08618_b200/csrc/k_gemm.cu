@@ -504,6 +504,26 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) schur_sym_kernel(
 // production configuration (chosen with tools/gemm_bench.py)
 using Prod = GemmCfg<64, 64, 32, 32, 2, false, 4>;
 
+// a group of independent clusters (disjoint Schur targets) in one launch: grid
+// tile t belongs to job tile_job[t] and is its (t - tile0)-th upper-triangle tile
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) schur_sym_multi_kernel(
+    const SchurJob *jobs, const int *tile_job) {
+    constexpr int BM = Cfg::BM, BN = Cfg::BN, FM = Cfg::FM, FN = Cfg::FN;
+    const SchurJob jb = jobs[tile_job[blockIdx.x]];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    constexpr int WCOLS = BN / Cfg::WN;
+    const int wm = (warp / WCOLS) * Cfg::WM, wn = (warp % WCOLS) * Cfg::WN;
+    int I, J;
+    tri_tile(blockIdx.x - jb.tile0, I, J);
+    const int z = blockIdx.y;
+    double acc[FM][FN][2];
+    tile_mainloop<Cfg>(jb.X + z * jb.sx, jb.ld, 0, jb.R, jb.Bg + z * jb.sx, jb.ld, 0, jb.R, jb.K,
+                       I * BM, J * BN, wm, wn, acc);
+    schur_sym_epilogue<Cfg, true>(acc, I * BM, J * BN, z, jb.R, jb.seg_of, jb.seg_start, jb.nseg,
+                                  jb.tbl);
+}
+
 template <class Cfg>
 void launch_cfg(const GemmTask *dev_tasks, const int *dev_tile_prefix, int ntasks,
                 int total_tiles, int nshift, cudaStream_t st) {
@@ -552,6 +572,14 @@ void launch_schur_sym(const double *X, const double *Bg, int64_t sx, int ld, int
         case 5: launch_sym<SymKP, 2>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, tiles, nshift, st); break;
         default: launch_sym<Prod, 2>(X, Bg, sx, ld, R, K, seg_of, seg_start, nseg, tbl, tiles, nshift, st);
     }
+}
+
+void launch_schur_sym_multi(const SchurJob *jobs, const int *tile_job, int total_tiles,
+                            int nshift, cudaStream_t st) {
+    if (total_tiles <= 0 || nshift <= 0) return;
+    smem_optin(schur_sym_multi_kernel<Prod>);
+    dim3 grid(total_tiles, nshift);
+    schur_sym_multi_kernel<Prod><<<grid, Prod::THREADS, Prod::SMEM, st>>>(jobs, tile_job);
 }
 
 int gemm_tiles(int M, int N) {

@@ -67,20 +67,23 @@ __device__ __forceinline__ void solve_regs(double *T, int S, const double *Ls, c
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) panel_kernel(const PanelTile *tiles, const double *L,
-                                                    int64_t lstride, int ldl, int n,
-                                                    const int *perm, const double *dinfo,
-                                                    int64_t pstride, double *W, double *X,
-                                                    int64_t wstride, int ldw, int lcw) {
+__global__ void __launch_bounds__(256) panel_kernel(const PanelTile *tiles, const PanelJob *jobs) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double colbuf[2][PANEL_ROWS];
+    const PanelTile tl = tiles[blockIdx.x];
+    const PanelJob jb = jobs[tl.job];
+    const double *L = jb.L;
+    const int64_t lstride = jb.lstride, pstride = jb.pstride, wstride = jb.wstride;
+    const int ldl = jb.ldl, n = jb.n, ldw = jb.ldw, lcw = jb.lcw;
+    const int *perm = jb.perm;
+    const double *dinfo = jb.dinfo;
+    double *W = jb.W, *X = jb.X;
+    const int z = blockIdx.y;
     const int S = n + 1 + (n & 1);  // odd row stride -> conflict-free column access
     double *T = sm;                 // PANEL_ROWS x S
     const bool lsm = n <= PANEL_L_SMEM;
     double *Ls = T + PANEL_ROWS * S;  // packed strictly-lower L by columns
     int *cs = (int *)(Ls + (lsm ? (int64_t)n * (n - 1) / 2 : 0));
-    const PanelTile tl = tiles[blockIdx.x];
-    const int z = blockIdx.y;
     const double *src = tl.src ? tl.src + z * tl.sstride : nullptr;
     const double *Lz = L + z * lstride;
     const int *pz = perm + z * pstride;
@@ -183,18 +186,13 @@ size_t panel_smem_bytes(int n) {
     return b;
 }
 
-cudaError_t launch_panel(const PanelTile *dev_tiles, int ntiles, int nshift, const double *L,
-                         int64_t lstride, int ldl, int n, const int *perm, const double *dinfo,
-                         int64_t pstride, double *W, double *X, int64_t wstride, int ldw,
-                         cudaStream_t st) {
-    if (ntiles <= 0 || nshift <= 0 || n <= 0) return cudaSuccess;
-    const size_t sm = panel_smem_bytes(n);
-    cudaError_t e =
-        smem_optin(panel_kernel);
+cudaError_t launch_panel_multi(const PanelTile *dev_tiles, int ntiles, int nshift,
+                               const PanelJob *dev_jobs, size_t smem_bytes, cudaStream_t st) {
+    if (ntiles <= 0 || nshift <= 0) return cudaSuccess;
+    cudaError_t e = smem_optin(panel_kernel);
     if (e != cudaSuccess) return e;
     dim3 grid(ntiles, nshift);
-    panel_kernel<<<grid, 256, sm, st>>>(dev_tiles, L, lstride, ldl, n, perm, dinfo, pstride, W, X,
-                                        wstride, ldw, panel_lcw(n));
+    panel_kernel<<<grid, 256, smem_bytes, st>>>(dev_tiles, dev_jobs);
     return cudaGetLastError();
 }
 

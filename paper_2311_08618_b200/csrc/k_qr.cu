@@ -248,10 +248,9 @@ namespace cg = cooperative_groups;
 constexpr int PQRC_THREADS = 256;
 
 template <int CS>
-__global__ void __launch_bounds__(PQRC_THREADS) pqr_cluster_kernel(double *Mg, int64_t mstride, int n,
-                                                                   double *tau, int *piv,
-                                                                   int64_t vstride,
-                                                                   const int *active, int kmax) {
+__device__ __forceinline__ void pqr_cluster_body(double *Mg, int64_t mstride, int n, double *tau,
+                                                 int *piv, int64_t vstride, const int *active,
+                                                 int kmax) {
     // One cluster barrier per column: every CTA proposes its best unused column
     // together with that column's Householder vector (double-buffered by step
     // parity), then all CTAs take the same winner, copy its vector through
@@ -443,17 +442,34 @@ __global__ void __launch_bounds__(PQRC_THREADS) pqr_cluster_kernel(double *Mg, i
     cluster.sync();  // no CTA exits while its shared memory may still be read
 }
 
+template <int CS>
+__global__ void __launch_bounds__(PQRC_THREADS) pqr_cluster_kernel(double *Mg, int64_t mstride, int n,
+                                                                   double *tau, int *piv,
+                                                                   int64_t vstride,
+                                                                   const int *active, int kmax) {
+    pqr_cluster_body<CS>(Mg, mstride, n, tau, piv, vstride, active, kmax);
+}
+
+// a group of clusters' Gram matrices in one launch: thread-block cluster c of the
+// grid row serves job c (all CTAs of a cluster read the same job: uniform exits)
+template <int CS>
+__global__ void __launch_bounds__(PQRC_THREADS) pqr_cluster_multi_kernel(const PqrJob *jobs,
+                                                                         const int *active) {
+    const PqrJob jb = jobs[blockIdx.x / CS];
+    if (jb.n <= 0) return;
+    pqr_cluster_body<CS>(jb.M, jb.mstride, jb.n, jb.tau, jb.piv, jb.vstride, active,
+                         jb.kmax <= 0 ? jb.n : min(jb.kmax, jb.n));
+}
+
 // Q^T of the reflectors in rows of V (row j: v_j = [1 at j, V[j][r] for r > j]):
 // row q of Q^T = (H_0 ... H_{n-1} e_q)^T, built by one warp from e_q with
 // H_j for j = min(q, n-1) .. 0 (H_j e_q = e_q for j > q).  Rows are independent,
 // so the grid spreads them over many CTAs and no barrier is needed.
 constexpr int FQ_WARPS = 8;
 
-__global__ void __launch_bounds__(FQ_WARPS * 32) form_q_rows_kernel(const double *V, int64_t vstr,
-                                                                   int n, const double *tau,
-                                                                   int64_t tstr, double *QT,
-                                                                   int64_t qstr,
-                                                                   const int *active, int kref) {
+__device__ __forceinline__ void form_q_rows_body(const double *V, int64_t vstr, int n,
+                                                 const double *tau, int64_t tstr, double *QT,
+                                                 int64_t qstr, const int *active, int kref) {
     extern __shared__ __align__(16) double ybuf[];
     const int z = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -481,6 +497,22 @@ __global__ void __launch_bounds__(FQ_WARPS * 32) form_q_rows_kernel(const double
         __syncwarp();
     }
     for (int r = lane; r < n; r += 32) out[r] = y[r];
+}
+
+__global__ void __launch_bounds__(FQ_WARPS * 32) form_q_rows_kernel(const double *V, int64_t vstr,
+                                                                   int n, const double *tau,
+                                                                   int64_t tstr, double *QT,
+                                                                   int64_t qstr,
+                                                                   const int *active, int kref) {
+    form_q_rows_body(V, vstr, n, tau, tstr, QT, qstr, active, kref);
+}
+
+__global__ void __launch_bounds__(FQ_WARPS * 32) form_q_rows_multi_kernel(const PqrJob *jobs,
+                                                                         const int *active) {
+    const PqrJob jb = jobs[blockIdx.z];
+    if (blockIdx.x * FQ_WARPS >= jb.n) return;
+    form_q_rows_body(jb.M, jb.mstride, jb.n, jb.tau, jb.vstride, jb.QT, jb.qstride, active,
+                     jb.kmax <= 0 ? jb.n : min(jb.kmax, jb.n));
 }
 
 size_t pqr_cluster_smem(int n, int cs) {
@@ -515,6 +547,34 @@ cudaError_t launch_pqr_cluster_cs(double *M, int64_t mstride, int n, double *tau
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, pqr_cluster_kernel<CS>, M, mstride, n, tau, piv, vstride, active,
                               kmax);
+}
+
+template <int CS>
+cudaError_t launch_pqr_cluster_multi_cs(const PqrJob *jobs, int njobs, int nmax, const int *active,
+                                        int nshift, cudaStream_t st) {
+    const size_t smem = pqr_cluster_smem(nmax, CS);
+    cudaError_t e = smem_optin(pqr_cluster_multi_kernel<CS>);
+    if (e != cudaSuccess) return e;
+    if (CS > 8) {
+        static std::once_flag once;
+        std::call_once(once, [] {
+            cudaFuncSetAttribute(pqr_cluster_multi_kernel<CS>,
+                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        });
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CS * njobs, nshift, 1);
+    cfg.blockDim = dim3(PQRC_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, pqr_cluster_multi_kernel<CS>, jobs, active);
 }
 
 }  // namespace
@@ -552,8 +612,25 @@ cudaError_t launch_form_q_rows(const double *V, int64_t vstride, int n, const do
     return cudaGetLastError();
 }
 
-namespace {
-}  // namespace
+cudaError_t launch_pqr_cluster_multi(const PqrJob *jobs, int njobs, int nmax, const int *active,
+                                     int nshift, cudaStream_t st) {
+    if (njobs <= 0 || nshift <= 0 || nmax <= 0) return cudaSuccess;
+    const int cs = pqr_cluster_size(nmax);
+    if (cs == 8) return launch_pqr_cluster_multi_cs<8>(jobs, njobs, nmax, active, nshift, st);
+    if (cs == 16) return launch_pqr_cluster_multi_cs<16>(jobs, njobs, nmax, active, nshift, st);
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_form_q_rows_multi(const PqrJob *jobs, int njobs, int nmax, const int *active,
+                                     int nshift, cudaStream_t st) {
+    if (njobs <= 0 || nshift <= 0 || nmax <= 0) return cudaSuccess;
+    const size_t smem = sizeof(double) * FQ_WARPS * (size_t)nmax;
+    cudaError_t e = smem_optin(form_q_rows_multi_kernel);
+    if (e != cudaSuccess) return e;
+    dim3 grid((nmax + FQ_WARPS - 1) / FQ_WARPS, nshift, njobs);
+    form_q_rows_multi_kernel<<<grid, FQ_WARPS * 32, smem, st>>>(jobs, active);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_pqr(double *GT, int64_t gstride, int c, int nR, int ldg, double *tau, int *piv,
                        int *used, double *norms, int64_t vstride, int64_t cstride,

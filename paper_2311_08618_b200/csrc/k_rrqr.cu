@@ -41,10 +41,9 @@ __global__ void __launch_bounds__(RR_THREADS) colenergy_kernel(const double *DT,
 // rank per shift: first r with sqrt(sum_{i>=r} e_i) <= tol (fixed-order sums);
 // also r1 = leading directions whose energy is >= 1e-10 of the first one (the
 // directions a Gram-based ordering resolves reliably), and the energies.
-__global__ void __launch_bounds__(RR_THREADS) tail_rank_kernel(const double *part, int nchunk, int n,
-                                                               const double *tol, int *rank,
-                                                               double *dropped, int *r1out,
-                                                               const int *active) {
+__device__ __forceinline__ void tail_rank_body(const double *part, int nchunk, int n,
+                                               const double *tol, int *rank, double *dropped,
+                                               int *r1out, const int *active) {
     extern __shared__ double e[];
     const int z = blockIdx.x;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -79,7 +78,56 @@ __global__ void __launch_bounds__(RR_THREADS) tail_rank_kernel(const double *par
     }
 }
 
+__global__ void __launch_bounds__(RR_THREADS) tail_rank_kernel(const double *part, int nchunk, int n,
+                                                               const double *tol, int *rank,
+                                                               double *dropped, int *r1out,
+                                                               const int *active) {
+    tail_rank_body(part, nchunk, n, tol, rank, dropped, r1out, active);
+}
+
+__global__ void __launch_bounds__(RR_THREADS) colenergy_multi_kernel(const RankJob *jobs,
+                                                                     int rows_per_chunk) {
+    const RankJob jb = jobs[blockIdx.z];
+    const int nchunk = max(1, (jb.c + rows_per_chunk - 1) / rows_per_chunk);
+    const int ch = blockIdx.x, z = blockIdx.y;
+    if (ch >= nchunk) return;
+    const double *D = jb.DT + z * jb.dstride;
+    const int q0 = ch * rows_per_chunk, q1 = min(jb.c, q0 + rows_per_chunk);
+    double *out = jb.part + ((int64_t)z * nchunk + ch) * jb.n;
+    for (int i = threadIdx.x; i < jb.n; i += blockDim.x) {
+        double s = 0.0;
+        for (int q = q0; q < q1; ++q) {
+            const double v = D[(int64_t)q * jb.n + i];
+            s += v * v;
+        }
+        out[i] = s;
+    }
+}
+
+__global__ void __launch_bounds__(RR_THREADS) tail_rank_multi_kernel(const RankJob *jobs,
+                                                                     int rows_per_chunk,
+                                                                     const double *tol,
+                                                                     const int *active) {
+    const RankJob jb = jobs[blockIdx.y];
+    const int nchunk = max(1, (jb.c + rows_per_chunk - 1) / rows_per_chunk);
+    tail_rank_body(jb.part, nchunk, jb.n, tol, jb.rank, jb.dropped, jb.r1, active);
+}
+
 }  // namespace
+
+cudaError_t launch_tail_rank_multi(const RankJob *jobs, int njobs, int cmax, int nmax,
+                                   const double *tol, const int *active, int nshift,
+                                   cudaStream_t st) {
+    if (njobs <= 0 || nmax <= 0 || nshift <= 0) return cudaSuccess;
+    const int rows = 256;
+    const int nchunk = std::max(1, (cmax + rows - 1) / rows);
+    colenergy_multi_kernel<<<dim3(nchunk, nshift, njobs), RR_THREADS, 0, st>>>(jobs, rows);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    tail_rank_multi_kernel<<<dim3(nshift, njobs), RR_THREADS, sizeof(double) * nmax, st>>>(
+        jobs, rows, tol, active);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_tail_rank(const double *DT, int64_t dstride, int c, int n, double *part,
                              const double *tol, int *rank, double *dropped, int *r1out,

@@ -270,6 +270,34 @@ def gershgorin_interval(A):
     return float((d - rad).min()), float((d + rad).max())
 
 
+def payload_digest(H):
+    """sha256 over the origin payload in a canonical order (bitwise identity of two H).
+
+    Works on this package's matrices and on the reference's `RankStructuredMatrix`
+    (same field names), so a fixture can pin a rebuilt H to the reference-built one."""
+    import hashlib
+
+    org = H.origin() if hasattr(H, "origin") else H
+    h = hashlib.sha256()
+
+    def put(tag, a):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        h.update(f"{tag}{a.shape}".encode())
+        h.update(a.tobytes())
+
+    for i in sorted(org.leaf_diag):
+        put(("D", i), org.leaf_diag[i])
+    for k in sorted(org.leaf_offdiag):
+        put(("O",) + tuple(k), org.leaf_offdiag[k])
+    for k in sorted(org.bases):
+        bs = org.bases[k]
+        put(("R",) + tuple(k), bs.U_R)
+        put(("S",) + tuple(k), bs.U_S)
+    for k in sorted(org.couplings):
+        put(("C",) + tuple(k), org.couplings[k])
+    return h.hexdigest()
+
+
 # ------------------------------------------------------------- payload file IO
 def save_payload(path, H):
     """Serialise the origin payload of H (tree ranges, structure, blocks) to .npz."""

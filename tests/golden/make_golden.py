@@ -267,10 +267,90 @@ def gen_mini():
     _record("mini_cfg1_1024", _ref_config_H("cfg1", 1024, 16), nshift=24)
 
 
+# ---------------------------------------------------------------- production-size
+# Same-recipe instances at each config's REAL leaf size (n = 16384): fronts of
+# 300-450 rows, rank growth by recompression, cluster BK, chunked panels and
+# large Gram orderings.  The payload is too large to commit (0.5-2 GB), so the
+# fixture stores a sha256 digest of the reference-built payload instead: the
+# GPU test rebuilds H with this package's host `construct` (bit-identical to the
+# reference's, checked against the digest) and factorizes THAT H on the device.
+PROD = (
+    # name, config, n, leaf, shifts, k for a reference slice_spectrum (0: none)
+    ("prod_cfg2_16k", "cfg2", 16384, 256, 12, 0),
+    ("prod_cfg3_16k", "cfg3", 16384, 256, 16, 8192),
+    ("prod_cfg4_16k", "cfg4", 16384, 256, 12, 0),
+    ("prod_cfg5_16k", "cfg5", 16384, 512, 16, 8192),
+)
+
+
+def gen_prod(only=()):
+    import time
+
+    from paper_2311_08618_b200.h2matrix import payload_digest
+
+    for name, cfgname, n, leaf, nshift, k in PROD:
+        if only and name not in only:
+            continue
+        t0 = time.perf_counter()
+        cfg = configs.CONFIGS[cfgname]
+        H = _ref_config_H(cfgname, n, leaf)
+        t_con = time.perf_counter() - t0
+        digest = payload_digest(H)
+        A = reconstruct_dense(H, cap=n)
+        w = np.linalg.eigvalsh(A)
+        del A
+        span = w[-1] - w[0]
+        nrm = max(abs(w[0]), abs(w[-1]))
+        rng = np.random.default_rng(11)
+        guard = 10 * H.eps * nrm
+        mus = []
+        while len(mus) < nshift:
+            if len(mus) % 3 == 0:
+                mu = float(rng.uniform(w[0] - 0.05 * span, w[-1] + 0.05 * span))
+            else:
+                i = int(rng.integers(0, len(w) - 1))
+                mu = float(w[i] + (w[i + 1] - w[i]) * rng.uniform(0.25, 0.75))
+            if np.min(np.abs(w - mu)) >= guard:
+                mus.append(mu)
+        counts, stats, secs = [], [], []
+        for mu in mus:
+            t1 = time.perf_counter()
+            f = generalized_ldl(shift_diagonal(H, mu))
+            secs.append(time.perf_counter() - t1)
+            c = f.inertia_counts
+            assert c.zero == 0, (name, mu)
+            counts.append((c.neg, c.zero, c.pos))
+            s = f.stats
+            stats.append((s["fill_blocks"], s["recompressions"], s["rank_added"], s["max_front"]))
+            print(name, f"mu={mu:.6g}", counts[-1], stats[-1], f"{secs[-1]:.1f}s", flush=True)
+        extra = {}
+        if k:
+            iv = (float(w[0]) - 1.0, float(w[-1]) + 1.0)
+            t1 = time.perf_counter()
+            est = slice_spectrum(H, k, iv, cfg.eps_ev, cache=InertiaCache())
+            extra = dict(est_k=np.array(k), est_interval=np.array(iv),
+                         estimate=np.array([est.value, est.half_width, est.iterations,
+                                            est.inertia_evals]),
+                         est_seconds=np.array(time.perf_counter() - t1))
+            print(name, "slice_spectrum k", k, est.value, "eigvalsh", w[k - 1],
+                  "iters", est.iterations, flush=True)
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), config=np.array(cfgname),
+                            n=np.array(n), leaf=np.array(leaf), digest=np.array(digest),
+                            scale0=np.array(H.scale_estimate()), mus=np.array(mus),
+                            counts=np.array(counts, dtype=np.int64),
+                            stats=np.array(stats, dtype=np.int64), eigs=w,
+                            ref_seconds=np.array(secs), construct_seconds=np.array(t_con),
+                            **extra)
+        print(name, "done: construct", f"{t_con:.1f}s", "digest", digest[:16], flush=True)
+
+
 if __name__ == "__main__":
     which = set(sys.argv[1:]) or {"bk", "sfc", "inst", "cfg1"}
     if "mini" in which:
         gen_mini()
+    prod = {w for w in which if w.startswith("prod")}
+    if prod:
+        gen_prod(() if "prod" in prod else tuple(prod))
     if "bk" in which:
         gen_bk()
     if "sfc" in which:

@@ -113,3 +113,92 @@ def test_sequential_and_multisection_agree_on_exact_counts():
                 else:
                     a = mu
             assert e.value == 0.5 * (a + b) and e.iterations == it, (batch, e.k)
+
+
+def _failing_worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    from paper_2311_08618_b200.multigpu import ShardError, multisection_distributed
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    w = _spectrum()
+    calls = [0]
+
+    def local_eval(mus):
+        calls[0] += 1
+        if rank == 1 and calls[0] == 2:
+            raise ValueError("injected device failure")
+        return _counts(w, mus)
+
+    try:
+        multisection_distributed(_Dummy(120), [60], (-40.0, 40.0), 1e-9, per_rank=7,
+                                 local_eval=local_eval)
+        out[rank] = "no error"
+    except ShardError:
+        out[rank] = "ShardError"
+    except ValueError as exc:
+        out[rank] = f"ValueError: {exc}"
+    dist.destroy_process_group()
+
+
+def test_failing_rank_raises_everywhere_without_hanging():
+    """a rank whose evaluation raises still joins the round's all-gather
+    (sentinel rows), so the other ranks raise ShardError instead of blocking."""
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_failing_worker, args=(r, world, port, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0
+    assert out[0] == "ShardError"
+    assert out[1] == "ValueError: injected device failure"
+
+
+def _static_worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    from paper_2311_08618_b200.multigpu import static_partition_distributed
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    w = _spectrum()
+    seen = []
+
+    def ev(mus):
+        seen.extend(mus)
+        return _counts(w, mus)
+
+    ests = static_partition_distributed(_Dummy(120), 55, 70, (-40.0, 40.0), 1e-9, per_sweep=15,
+                                        evaluate=ev)
+    out[rank] = ([(e.k, e.value, e.iterations) for e in ests], len(seen))
+    dist.destroy_process_group()
+
+
+def test_k_sharded_static_partition_identical_to_serial():
+    """cfg4-style index range: contiguous k chunks per rank (parallel.py:85-96),
+    private caches, one all-gather of the estimates; identical to serial."""
+    w = _spectrum()
+    serial = bisection.multisection(_Dummy(120), list(range(55, 71)), (-40.0, 40.0), 1e-9,
+                                    batch=15, evaluate=lambda mus: _counts(w, mus))
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_static_worker, args=(r, world, port, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0
+    want = [(e.k, e.value, e.iterations) for e in serial]
+    assert out[0][0] == out[1][0] == want
+    assert out[0][1] > 0 and out[1][1] > 0
