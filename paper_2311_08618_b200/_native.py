@@ -110,6 +110,25 @@ def load_library(path=LIB_PATH):
         return lib
 
 
+TESTING_LIB_PATH = os.path.join(os.path.dirname(LIB_PATH), "libh2ldl_testing.so")
+_tlib = None
+
+
+def load_testing_library(path=TESTING_LIB_PATH):
+    """libh2ldl_testing.so: test / benchmark entry points outside the product ABI
+    (GEMM tile variants, BK and Gram-ordering kernels on host matrices, the INT8
+    Ozaki Schur kernel on dense inputs).  Only tests/ and tools/ load it."""
+    global _tlib
+    load_library()
+    with _lib_lock:
+        if _tlib is None:
+            if not os.path.exists(path):
+                raise NativeError(f"{path} is missing: run __graft_entry__.build()")
+            _tlib = ctypes.CDLL(path)
+            _tlib.h2l_testing_last_error.restype = ctypes.c_char_p
+        return _tlib
+
+
 def _check(rc, handle=None, what=""):
     if rc != H2L_OK:
         msg = load_library().h2l_last_error(handle)

@@ -166,6 +166,28 @@ struct SchurTarget {
     int ldc, trans;
 };
 int schur_sym_tiles(int R);
+
+// fire-and-forget global fp64 add (RED.E.ADD.F64 in L2)
+__device__ __forceinline__ void red_add_f64(double *p, double v) {
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "d"(v) : "memory");
+}
+
+// one cluster of the INT8-tensor-core (Ozaki) Schur update (k_schur_oz.cu): its
+// X / Bg rows are packed at rows [row0, row0 + round_up(R, 128)) of the slice buffers
+struct OzJob {
+    const double *X, *Bg;
+    int64_t sx;
+    int ld, R, K, nseg;
+    const int *seg_of, *seg_start;   // seg_of == nullptr: one segment, dense target (tests)
+    const SchurTarget *tbl;
+    int row0;          // first packed row
+    int tile0;         // first grid tile
+};
+int schur_oz_tiles(int R);
+size_t schur_oz_scratch_bytes(int rows_total, int kpad, int nshift);
+cudaError_t launch_schur_oz(const OzJob *jobs, const int *row_job, const int *tile_job,
+                            int rows_total, int kpad, int total_tiles, int nshift, void *scratch,
+                            cudaStream_t st, double *dense_out = nullptr, int ld_out = 0);
 void launch_schur_sym(const double *X, const double *Bg, int64_t sx, int ld, int R, int K,
                       const int *seg_of, const int *seg_start, int nseg, const SchurTarget *tbl,
                       int nshift, cudaStream_t st, int variant = 0);

@@ -41,22 +41,9 @@
 #include <vector>
 
 #include "common.cuh"
-#include "../../include/h2ldl.h"
+#include "host_util.h"
 
 namespace h2l {
-
-struct CudaFail : std::runtime_error {
-    int code;
-    CudaFail(int c, const std::string &m) : std::runtime_error(m), code(c) {}
-};
-
-#define CK(x)                                                                              \
-    do {                                                                                   \
-        cudaError_t e_ = (x);                                                              \
-        if (e_ != cudaSuccess)                                                             \
-            throw ::h2l::CudaFail(e_ == cudaErrorMemoryAllocation ? H2L_ENOMEM : H2L_ECUDA,       \
-                           std::string(#x) + ": " + cudaGetErrorString(e_));                \
-    } while (0)
 
 using Pair = std::pair<int, int>;
 
@@ -145,6 +132,7 @@ public:
         else if (k == "window") window_ = (int)std::max<int64_t>(1, v);
         else if (k == "group_mem_mb") group_mem_mb_ = std::max<int64_t>(1, v);
         else if (k == "group_max") group_max_ = (int)std::max<int64_t>(1, v);
+        else if (k == "schur_arith") schur_arith_ = v == 1 ? 1 : 0;
         else throw CudaFail(H2L_EINVAL, "unknown option " + k);
     }
 
@@ -270,7 +258,7 @@ public:
         ranges_ = o.ranges_; boff_ = o.boff_; brank_ = o.brank_; bdim_ = o.bdim_;
         dense_ = o.dense_; lowrank_ = o.lowrank_; deferred_ = o.deferred_; coup_off_ = o.coup_off_;
         arena_ = o.arena_; skel_ = o.skel_; skel_diag_ = o.skel_diag_; skel_off_ = o.skel_off_;
-        max_batch_ = o.max_batch_; time_kernels_ = o.time_kernels_; schedule_ = o.schedule_; window_ = o.window_; group_mem_mb_ = o.group_mem_mb_; group_max_ = o.group_max_; elim_order_ = o.elim_order_; qr_budget_ = o.qr_budget_; block_cache_ = o.block_cache_;
+        max_batch_ = o.max_batch_; time_kernels_ = o.time_kernels_; schedule_ = o.schedule_; window_ = o.window_; group_mem_mb_ = o.group_mem_mb_; group_max_ = o.group_max_; elim_order_ = o.elim_order_; qr_budget_ = o.qr_budget_; block_cache_ = o.block_cache_; schur_arith_ = o.schur_arith_;
         owns_payload_ = false;
         uploaded_ = o.uploaded_;
     }
@@ -337,6 +325,7 @@ private:
     int group_max_ = 512;
     int t_level_max_ = -1;  // largest recompression rank of the current level (-1: none yet)
     bool qr_budget_ = true;
+    int schur_arith_ = 0;             // 0 DMMA fp64, 1 INT8 tensor cores, Ozaki slices (k_schur_oz.cu)
     bool uploaded_ = false;
     cudaEvent_t ev_call_[2];
     std::vector<cudaEvent_t> ev_pool_;
@@ -1767,6 +1756,10 @@ private:
             // space, scattered to the target blocks (fill blocks created on demand,
             // zeroed in one batched launch first: gldl.py:398-409)
             CopyBatch fz;
+            const bool oz = schur_arith_ == 1;
+            std::vector<OzJob> ozj;
+            std::vector<int> row_job;
+            int oz_rows = 0, oz_kpad = 0;
             std::vector<SchurJob> sj;
             std::vector<int> seg_all, start_all, tile_job;
             std::vector<SchurTarget> tbl_all;
@@ -1827,16 +1820,28 @@ private:
                             e.base = T->at(a.lo, b.lo); e.bs = T->bs; e.ldc = T->cols;
                         }
                     }
-                const int tl = schur_sym_tiles(j.R);
+                const int tl = oz ? schur_oz_tiles(j.R) : schur_sym_tiles(j.R);
                 sj.push_back(SchurJob{j.Xb.p, j.Bg.p, j.Xb.bs, nR, j.R, nR, ns, nullptr, nullptr, nullptr,
                                       tiles_tot, 0});
+                if (oz) {
+                    OzJob o{};
+                    o.X = j.Xb.p; o.Bg = j.Bg.p; o.sx = j.Xb.bs; o.ld = nR; o.R = j.R; o.K = nR;
+                    o.nseg = ns; o.row0 = oz_rows; o.tile0 = tiles_tot;
+                    ozj.push_back(o);
+                    const int rp = (j.R + 127) / 128;
+                    row_job.insert(row_job.end(), rp, (int)ozj.size() - 1);
+                    oz_rows += 128 * rp;
+                    oz_kpad = std::max(oz_kpad, (nR + 63) / 64 * 64);
+                }
                 tile_job.insert(tile_job.end(), tl, (int)sj.size() - 1);
                 tiles_tot += tl;
                 // algorithmic panel work (survey §8d): TRSM R nR^2 + D-scale R nR
                 flops_tot += (double)j.R * nR * nR + (double)j.R * nR + sch;
                 sch_tot += sch;
                 bytes_tot += sch_bytes;
-                st_acc_->gemm_flops_exec += 2.0 * (double)tl * 64 * 64 * nR * s_;
+                // executed tensor work (fp64-equivalent 2MNK of the padded tiles)
+                st_acc_->gemm_flops_exec += oz ? 2.0 * (double)tl * 128 * 64 * ((nR + 63) / 64 * 64) * s_
+                                               : 2.0 * (double)tl * 64 * 64 * nR * s_;
             }
             flush(fz);
             // one staged region: segment maps, target tables, tile->job map, job table
@@ -1847,21 +1852,39 @@ private:
             const size_t otb = pk2.add(tbl_all.data(), sizeof(SchurTarget) * tbl_all.size());
             const size_t otj = pk2.add(tile_job.data(), sizeof(int) * tile_job.size());
             const size_t osj = pk2.add(sj.data(), sizeof(SchurJob) * sj.size());
+            const size_t ooz = oz ? pk2.add(ozj.data(), sizeof(OzJob) * ozj.size()) : 0;
+            const size_t orj = oz ? pk2.add(row_job.data(), sizeof(int) * row_job.size()) : 0;
             StageRegion rg = stage_begin(pk2.h.size());
             SchurJob *hj = (SchurJob *)(pk2.h.data() + osj);
+            OzJob *ho = oz ? (OzJob *)(pk2.h.data() + ooz) : nullptr;
             for (size_t q = 0; q < sj.size(); ++q) {
                 hj[q].seg_of = (const int *)(rg.d + os) + seg_off[q];
                 hj[q].seg_start = (const int *)(rg.d + ost) + start_off[q];
                 hj[q].tbl = (const SchurTarget *)(rg.d + otb) + tbl_off[q];
+                if (ho) {
+                    ho[q].seg_of = hj[q].seg_of;
+                    ho[q].seg_start = hj[q].seg_start;
+                    ho[q].tbl = hj[q].tbl;
+                }
             }
             std::memcpy(rg.h, pk2.h.data(), pk2.h.size());
             stage_commit(rg);
             char *d2 = rg.d;
+            void *scratch = nullptr;
+            if (oz)
+                CK(cudaMallocFromPoolAsync(&scratch, schur_oz_scratch_bytes(oz_rows, oz_kpad, s_), pool_,
+                                           st_));
             {
                 Timed tm(this, 1);
-                launch_schur_sym_multi((const SchurJob *)(d2 + osj), (const int *)(d2 + otj), tiles_tot,
-                                       s_, st_);
+                if (oz)
+                    CK(launch_schur_oz((const OzJob *)(d2 + ooz), (const int *)(d2 + orj),
+                                       (const int *)(d2 + otj), oz_rows, oz_kpad, tiles_tot, s_, scratch,
+                                       st_));
+                else
+                    launch_schur_sym_multi((const SchurJob *)(d2 + osj), (const int *)(d2 + otj),
+                                           tiles_tot, s_, st_);
             }
+            if (scratch) CK(cudaFreeAsync(scratch, st_));
             CK(cudaGetLastError());
             dbg_sync("schur-sym");
             st_acc_->launches++;
@@ -2696,259 +2719,3 @@ int h2l_inertia_multi(h2l_comm *comm, const double *mu, int32_t s_total, int64_t
 
 }  // extern "C"
 
-// ------------------------------------------------------------ internal tooling
-// Not part of the ABI (absent from h2ldl.h): micro-benchmark of the DMMA GEMM
-// tile variants on a Schur-shaped grouped workload (tools/gemm_bench.py).
-namespace h2l {
-int gemm_variant_tiles(int v, int M, int N);
-void launch_gemm_variant(int v, const GemmTask *dev_tasks, const int *dev_tile_prefix, int ntasks,
-                         int total_tiles, int nshift, cudaStream_t st);
-}
-
-extern "C" int h2l_internal_gemm_bench(int device, int variant, int M, int N, int K, int ntasks,
-                                       int nshift, int reps, double *ms_out, double *maxdiff_out) {
-    return guarded(nullptr, [&] {
-        CK(cudaSetDevice(device));
-        const int64_t sa = (int64_t)M * K, sb = (int64_t)N * K, sc = (int64_t)M * N;
-        const int64_t per = (sa + sb + sc) * ntasks;
-        double *buf, *ref;
-        CK(cudaMalloc(&buf, sizeof(double) * per * nshift));
-        CK(cudaMalloc(&ref, sizeof(double) * sc * ntasks * nshift));
-        std::vector<double> h(per * nshift);
-        uint64_t x = 88172645463325252ull;
-        for (auto &v : h) { x ^= x << 13; x ^= x >> 7; x ^= x << 17; v = (double)(x % 2001) / 1000.0 - 1.0; }
-        CK(cudaMemcpy(buf, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
-        std::vector<h2l::GemmTask> tasks(ntasks);
-        for (int t = 0; t < ntasks; ++t) {
-            h2l::GemmTask &g = tasks[t];
-            g = h2l::GemmTask{};
-            g.A = buf + t * sa; g.B = buf + ntasks * sa + t * sb; g.C = buf + ntasks * (sa + sb) + t * sc;
-            g.sA = g.sB = g.sC = per;
-            g.M = M; g.N = N; g.K = K; g.lda = K; g.ldb = K; g.ldc = N; g.tA = 0; g.tB = 1;
-            g.alpha = -1.0; g.beta = 1.0;
-        }
-        auto run = [&](int v, int nrep, float *ms) {
-            std::vector<int> pre(ntasks);
-            int tiles = 0;
-            for (int t = 0; t < ntasks; ++t) { pre[t] = tiles; tiles += h2l::gemm_variant_tiles(v, M, N); }
-            h2l::GemmTask *dt; int *dp;
-            CK(cudaMalloc(&dt, sizeof(h2l::GemmTask) * ntasks));
-            CK(cudaMalloc(&dp, sizeof(int) * ntasks));
-            CK(cudaMemcpy(dt, tasks.data(), sizeof(h2l::GemmTask) * ntasks, cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(dp, pre.data(), sizeof(int) * ntasks, cudaMemcpyHostToDevice));
-            cudaEvent_t e0, e1;
-            cudaEventCreate(&e0); cudaEventCreate(&e1);
-            h2l::launch_gemm_variant(v, dt, dp, ntasks, tiles, nshift, 0);  // warm
-            CK(cudaDeviceSynchronize());
-            cudaEventRecord(e0);
-            for (int r = 0; r < nrep; ++r) h2l::launch_gemm_variant(v, dt, dp, ntasks, tiles, nshift, 0);
-            cudaEventRecord(e1);
-            CK(cudaEventSynchronize(e1));
-            cudaEventElapsedTime(ms, e0, e1);
-            cudaEventDestroy(e0); cudaEventDestroy(e1);
-            cudaFree(dt); cudaFree(dp);
-        };
-        // correctness: one launch of `variant` vs one of variant 0 from the same inputs
-        const size_t cbytes = sizeof(double) * sc * ntasks;
-        std::vector<double> c0(sc * ntasks), c1(sc * ntasks);
-        double *Cz = buf + ntasks * (sa + sb);
-        float ms = 0.f;
-        CK(cudaMemcpy(ref, Cz, cbytes, cudaMemcpyDeviceToDevice));
-        run(0, 0, &ms);
-        CK(cudaMemcpy(c0.data(), Cz, cbytes, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(Cz, ref, cbytes, cudaMemcpyDeviceToDevice));
-        run(variant, 0, &ms);
-        CK(cudaMemcpy(c1.data(), Cz, cbytes, cudaMemcpyDeviceToHost));
-        double md = 0.0;
-        for (size_t q = 0; q < c0.size(); ++q) md = std::max(md, std::fabs(c0[q] - c1[q]));
-        run(variant, reps, &ms);
-        *ms_out = ms / std::max(1, reps);
-        *maxdiff_out = md;
-        cudaFree(buf); cudaFree(ref);
-    });
-}
-
-// Debug: production GEMM vs a naive reference kernel on a Schur-shaped
-// grouped workload; returns the max abs difference (tools/gemm_concurrency.py).
-namespace h2l {
-__global__ void naive_gemm_kernel(const GemmTask *tasks, int ntasks) {
-    const int t = blockIdx.x, z = blockIdx.y;
-    if (t >= ntasks) return;
-    const GemmTask tk = tasks[t];
-    const double *A = tk.A + z * tk.sA, *B = tk.B + z * tk.sB;
-    double *C = tk.C + z * tk.sC;
-    for (int e = threadIdx.x; e < tk.M * tk.N; e += blockDim.x) {
-        const int r = e / tk.N, c = e % tk.N;
-        double s = 0.0;
-        for (int k = 0; k < tk.K; ++k) {
-            const double a = tk.tA ? A[(int64_t)k * tk.lda + r] : A[(int64_t)r * tk.lda + k];
-            const double b = tk.tB ? B[(int64_t)c * tk.ldb + k] : B[(int64_t)k * tk.ldb + c];
-            s += a * b;
-        }
-        C[(int64_t)r * tk.ldc + c] = tk.alpha * s + tk.beta * C[(int64_t)r * tk.ldc + c];
-    }
-}
-}  // namespace h2l
-
-// Gram-matrix ordering of the recompression (k_qr.cu): `count` symmetric n x n
-// matrices (host, row-major) -> Q^T (count x n x n), tau, piv; mode 0 the cluster
-// kernel pair, mode 1 the single-CTA fallback pair
-extern "C" int h2l_internal_gram_order(int device, int mode, int n, int count, const double *m,
-                                       double *qt, double *tau, int *piv) {
-    return guarded(nullptr, [&] {
-        CK(cudaSetDevice(device));
-        const int64_t nn = (int64_t)n * n, ts = n;
-        double *dm, *dq, *dt, *dnorm, *dtol, *ddrop;
-        int *dp, *du, *drank;
-        CK(cudaMalloc(&dm, sizeof(double) * nn * count));
-        CK(cudaMalloc(&dq, sizeof(double) * nn * count));
-        CK(cudaMalloc(&dt, sizeof(double) * ts * count));
-        CK(cudaMalloc(&dnorm, sizeof(double) * ts * count));
-        CK(cudaMalloc(&dtol, sizeof(double) * count));
-        CK(cudaMalloc(&ddrop, sizeof(double) * count));
-        CK(cudaMalloc(&dp, sizeof(int) * ts * count));
-        CK(cudaMalloc(&du, sizeof(int) * ts * count));
-        CK(cudaMalloc(&drank, sizeof(int) * count));
-        CK(cudaMemcpy(dm, m, sizeof(double) * nn * count, cudaMemcpyHostToDevice));
-        CK(cudaMemset(dtol, 0, sizeof(double) * count));
-        if (mode == 0) {
-            if (!h2l::pqr_cluster_size(n)) throw h2l::CudaFail(H2L_EINVAL, "n too large for the cluster QR");
-            CK(h2l::launch_pqr_cluster(dm, nn, n, dt, dp, ts, nullptr, count, 0));
-            CK(h2l::launch_form_q_rows(dm, nn, n, dt, ts, dq, nn, nullptr, count, 0));
-        } else {
-            CK(h2l::launch_pqr(dm, nn, n, n, n, dt, dp, du, dnorm, ts, ts, dtol, drank, ddrop, nullptr,
-                               -2, count, 0));
-            CK(h2l::launch_form_tr(dm, nn, n, dt, dp, ts, n, n, dq, nn, nullptr, count, 0));
-        }
-        CK(cudaDeviceSynchronize());
-        CK(cudaMemcpy(qt, dq, sizeof(double) * nn * count, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(tau, dt, sizeof(double) * ts * count, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(piv, dp, sizeof(int) * ts * count, cudaMemcpyDeviceToHost));
-        for (void *p : {(void *)dm, (void *)dq, (void *)dt, (void *)dnorm, (void *)dtol, (void *)ddrop,
-                        (void *)dp, (void *)du, (void *)drank})
-            cudaFree(p);
-    });
-}
-
-// engine-mode BK of `count` n x n row-major matrices (host), single-CTA (mode 0)
-// or cluster (mode 1) kernel: factor (lower triangle), perm, dinfo, counts, status
-extern "C" int h2l_internal_bk_engine(int device, int mode, int n, int count, double *a, int *perm,
-                                      double *dinfo, int64_t *counts, int *status) {
-    return guarded(nullptr, [&] {
-        CK(cudaSetDevice(device));
-        const int64_t nn = (int64_t)n * n, ps = n;
-        double *da, *dd, *scr = nullptr;
-        int *dp, *dst;
-        int64_t *dc;
-        h2l::BkJob *dj;
-        CK(cudaMalloc(&da, sizeof(double) * nn * count));
-        CK(cudaMalloc(&dd, sizeof(double) * 3 * ps * count));
-        CK(cudaMalloc(&dp, sizeof(int) * ps * count));
-        CK(cudaMalloc(&dst, sizeof(int) * count));
-        CK(cudaMalloc(&dc, sizeof(int64_t) * 3 * count));
-        CK(cudaMalloc(&dj, sizeof(h2l::BkJob)));
-        CK(cudaMemcpy(da, a, sizeof(double) * nn * count, cudaMemcpyHostToDevice));
-        CK(cudaMemset(dst, 0, sizeof(int) * count));
-        CK(cudaMemset(dc, 0, sizeof(int64_t) * 3 * count));
-        h2l::BkJob jb{da, nn, n, n, dp, dd, ps};
-        CK(cudaMemcpy(dj, &jb, sizeof(jb), cudaMemcpyHostToDevice));
-        if (mode == 1) {
-            if (!h2l::bk_cluster_size(n)) throw h2l::CudaFail(H2L_EINVAL, "n too large for the cluster BK");
-            CK(h2l::launch_bk_cluster(dj, 1, count, n, dc, dst, 0));
-        } else {
-            const int64_t sd = h2l::bk_scratch_doubles(n);
-            if (sd) CK(cudaMalloc(&scr, sizeof(double) * sd * count));
-            CK(h2l::launch_bk_engine(dj, 1, count, n, dc, dst, scr, sd, 0));
-        }
-        CK(cudaDeviceSynchronize());
-        CK(cudaMemcpy(a, da, sizeof(double) * nn * count, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(perm, dp, sizeof(int) * ps * count, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(dinfo, dd, sizeof(double) * 3 * ps * count, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(counts, dc, sizeof(int64_t) * 3 * count, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(status, dst, sizeof(int) * count, cudaMemcpyDeviceToHost));
-        for (void *p : {(void *)da, (void *)dd, (void *)dp, (void *)dst, (void *)dc, (void *)dj})
-            cudaFree(p);
-        if (scr) cudaFree(scr);
-    });
-}
-
-extern "C" int h2l_internal_gemm_check(int device, int M, int N, int K, int ntasks, int nshift,
-                                       int reps, double *maxdiff_out) {
-    return guarded(nullptr, [&] {
-        CK(cudaSetDevice(device));
-        cudaStream_t st;
-        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-        const int64_t sa = (int64_t)M * K, sb = (int64_t)N * K, sc = (int64_t)M * N;
-        const int64_t per = (sa + sb + 2 * sc) * ntasks;
-        double *buf;
-        CK(cudaMalloc(&buf, sizeof(double) * per * nshift));
-        std::vector<double> h(per * nshift);
-        uint64_t x = 0x9E3779B97F4A7C15ull ^ (uint64_t)(M * 131 + N * 7 + ntasks);
-        for (auto &v : h) { x ^= x << 13; x ^= x >> 7; x ^= x << 17; v = (double)(x % 2001) / 1000.0 - 1.0; }
-        CK(cudaMemcpy(buf, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
-        std::vector<h2l::GemmTask> t1(ntasks), t2(ntasks);
-        std::vector<int> pre(ntasks);
-        int tiles = 0;
-        for (int t = 0; t < ntasks; ++t) {
-            h2l::GemmTask g{};
-            g.A = buf + t * sa; g.B = buf + ntasks * sa + t * sb;
-            g.sA = g.sB = g.sC = per;
-            g.M = M; g.N = N; g.K = K; g.lda = K; g.ldb = K; g.ldc = N; g.tA = 0; g.tB = 1;
-            g.alpha = -1.0; g.beta = 1.0;
-            g.C = buf + ntasks * (sa + sb) + t * sc;
-            t1[t] = g;
-            g.C = buf + ntasks * (sa + sb + sc) + t * sc;
-            t2[t] = g;
-            pre[t] = tiles;
-            tiles += h2l::gemm_tiles(M, N);
-        }
-        h2l::GemmTask *d1, *d2; int *dp;
-        CK(cudaMalloc(&d1, sizeof(h2l::GemmTask) * ntasks));
-        CK(cudaMalloc(&d2, sizeof(h2l::GemmTask) * ntasks));
-        CK(cudaMalloc(&dp, sizeof(int) * ntasks));
-        CK(cudaMemcpy(d1, t1.data(), sizeof(h2l::GemmTask) * ntasks, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(d2, t2.data(), sizeof(h2l::GemmTask) * ntasks, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(dp, pre.data(), sizeof(int) * ntasks, cudaMemcpyHostToDevice));
-        // both C copies start equal (copy C1 -> C2)
-        for (int z = 0; z < nshift; ++z)
-            CK(cudaMemcpyAsync(buf + z * per + ntasks * (sa + sb + sc), buf + z * per + ntasks * (sa + sb),
-                               sizeof(double) * sc * ntasks, cudaMemcpyDeviceToDevice, st));
-        CK(cudaStreamSynchronize(st));
-        double md = 0.0;
-        for (int r = 0; r < reps; ++r) {
-            h2l::launch_gemm(d1, dp, ntasks, tiles, nshift, st);
-            cudaError_t e1 = cudaGetLastError();
-            h2l::naive_gemm_kernel<<<dim3(ntasks, nshift), 256, 0, st>>>(d2, ntasks);
-            cudaError_t e2 = cudaGetLastError();
-            cudaError_t e3 = cudaStreamSynchronize(st);
-            if (e1 || e2 || e3)
-                fprintf(stderr, "LAUNCH rep %d: gemm=%s naive=%s sync=%s\n", r, cudaGetErrorString(e1),
-                        cudaGetErrorString(e2), cudaGetErrorString(e3));
-        }
-        std::vector<double> c1(sc * ntasks * nshift), c2(sc * ntasks * nshift);
-        for (int z = 0; z < nshift; ++z) {
-            CK(cudaMemcpy(c1.data() + z * sc * ntasks, buf + z * per + ntasks * (sa + sb),
-                          sizeof(double) * sc * ntasks, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(c2.data() + z * sc * ntasks, buf + z * per + ntasks * (sa + sb + sc),
-                          sizeof(double) * sc * ntasks, cudaMemcpyDeviceToHost));
-        }
-        int64_t nbad = 0;
-        for (size_t q = 0; q < c1.size(); ++q) {
-            const double d = std::fabs(c1[q] - c2[q]);
-            md = std::max(md, d);
-            if (d > 1e-9) {
-                if (nbad < 12) {
-                    const int64_t z = q / (sc * ntasks), rem = q % (sc * ntasks);
-                    const int64_t t = rem / sc, e = rem % sc;
-                    fprintf(stderr, "BAD z=%lld task=%lld r=%lld c=%lld got=%g want=%g\n", (long long)z,
-                            (long long)t, (long long)(e / N), (long long)(e % N), c1[q], c2[q]);
-                }
-                ++nbad;
-            }
-        }
-        if (nbad) fprintf(stderr, "BAD total %lld of %zu\n", (long long)nbad, c1.size());
-        *maxdiff_out = md;
-        cudaFree(buf); cudaFree(d1); cudaFree(d2); cudaFree(dp);
-        cudaStreamDestroy(st);
-    });
-}

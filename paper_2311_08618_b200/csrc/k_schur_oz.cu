@@ -1,0 +1,447 @@
+// K6 Schur update  C_big -= X Bg^T  on the INT8 tensor cores (tcgen05.mma.kind::i8),
+// fp64-accurate by exact integer slicing (the Ozaki scheme).
+//
+// Blackwell has no fp64 tcgen05 kind; the fp64 path is DMMA through mma.sync at
+// ~37 TF/s (k_gemm.cu schur_sym_kernel).  The INT8 tensor pipe is 4.5 POPS dense.
+// Every row r of X (and of Bg) is written exactly as
+//     x_rk = 2^e_r * sum_{p<8} 2^{-7(p+1)} s_rkp ,   s_rkp in [-127, 127]
+// (e_r = exponent of the row's largest entry; each slice peels 7 bits; the residual
+// after 8 slices is < 2^-56 of the row maximum, below fp64's 53-bit mantissa).
+// Then (X Bg^T)_rc = 2^(e_r + e_c) sum_{i,j} 2^{-7(i+j+2)} (S_i T_j^T)_rc, each slice
+// product exact in int32 (|sum| <= 127^2 K < 2^31 for K <= 2^17).  Pairs with
+// i + j <= 7 are kept (36 of 64; the dropped tail is < 2^-63 of the row/column
+// maxima), and all pairs of one i + j = g share one int32 accumulator in tensor
+// memory: 8 groups x 64 columns = the SM's 512 TMEM columns.  The epilogue sums
+// the 8 group totals in fp64 (smallest first) and applies the row/column exponents;
+// the only roundings are those of that final 8-term fp64 sum -- fewer than the
+// K-term fp64 dot product of the DMMA kernel.
+//
+// Kernel structure (one CTA per 128 x 64 upper-triangle tile x shift, 1 CTA/SM):
+//   warp 0      TMA producer: per 64-byte K block, the 8 slices of the X rows
+//               (8 x 128 x 64 B) and of the Bg rows (8 x 64 x 64 B), SWIZZLE_64B,
+//               double-buffered (2 x 96 KB);
+//   warp 1      TMEM allocation + MMA issue (one thread): 36 pairs x 2 K-steps of
+//               M=128, N=64, K=32 per stage, tcgen05.commit frees the stage;
+//   warps 2..9  epilogue: tcgen05.ld of the 8 group accumulators, fp64 sum, tile
+//               staged in shared memory, then the segment-pair scatter of
+//               schur_sym_kernel (fire-and-forget RED.ADD.F64, one writer per
+//               element), row-contiguous so a warp's reductions hit one row.
+// Reference: the Schur update of the elimination, gldl.py:388-409.
+#include <cuda.h>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace h2l {
+
+namespace oz {
+
+constexpr int SLICES = 8;
+constexpr int BM = 128, BN = 64, BKB = 64;           // tile rows, tile cols, K bytes per stage
+constexpr int A_SLICE = BM * BKB, B_SLICE = BN * BKB;  // 8 KB, 4 KB
+constexpr int STAGE = SLICES * (A_SLICE + B_SLICE);    // 96 KB
+constexpr int NSTAGE = 2;
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 64 + 32 * EPI_WARPS;           // 320
+constexpr int CT_LD = BN + 1;                          // staged tile row stride (doubles)
+constexpr int SMEM = NSTAGE * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+static_assert(BM * CT_LD * 8 <= NSTAGE * STAGE, "staged tile fits the pipeline buffers");
+
+__device__ __forceinline__ uint32_t su32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n\t}" ::"r"(su32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0,
+                                            int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(su32(dst)),
+        "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     su32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                       uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// K-major operand tile with 64-byte swizzle: rows of 64 bytes, 8-row groups 512 B apart
+__device__ __forceinline__ uint64_t sdesc_sw64(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address
+    d |= (uint64_t)1 << 16;                          // leading byte offset (unused: swizzled K-major)
+    d |= (uint64_t)(512 >> 4) << 32;                 // stride byte offset: next 8-row group
+    d |= (uint64_t)1 << 46;                          // descriptor version (sm_100)
+    d |= (uint64_t)4 << 61;                          // SWIZZLE_64B
+    return d;
+}
+// instruction descriptor: kind::i8, s32 accumulate, signed A/B, both K-major, M=128, N=64
+constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+          "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+          "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// tile t of a job with R rows -> (I, J): row tile I (128), column tile J (64), J >= 2I
+__device__ __forceinline__ void tri_tile_oz(int t, int R, int &I, int &J) {
+    const int NJ = (R + BN - 1) / BN;
+    I = 0;
+    while (true) {
+        const int cnt = NJ - 2 * I;
+        if (t < cnt) {
+            J = 2 * I + t;
+            return;
+        }
+        t -= cnt;
+        ++I;
+    }
+}
+
+}  // namespace oz
+
+int schur_oz_tiles(int R) {
+    if (R <= 0) return 0;
+    const int NI = (R + oz::BM - 1) / oz::BM, NJ = (R + oz::BN - 1) / oz::BN;
+    int n = 0;
+    for (int I = 0; I < NI; ++I) n += NJ - 2 * I > 0 ? NJ - 2 * I : 0;
+    return n;
+}
+
+// --------------------------------------------------------------------- slicing
+// rows of X (which = 0) / Bg (which = 1) of every job -> 8 int8 slices + row exponent.
+// One warp per row; grid (row blocks of 8 rows over the packed rows, shifts, 2).
+__global__ void __launch_bounds__(256) oz_split_kernel(const OzJob *jobs, const int *row_job,
+                                                       int rows_total, int kpad, int8_t *sx_out,
+                                                       int8_t *sb_out, int *ex_out, int *eb_out) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row = blockIdx.x * 8 + warp;
+    if (row >= rows_total) return;
+    const int z = blockIdx.y, which = blockIdx.z;
+    const OzJob jb = jobs[row_job[row / oz::BM]];
+    const int r = row - jb.row0;
+    int8_t *out = (which ? sb_out : sx_out) + ((size_t)z * oz::SLICES * rows_total + row) * kpad;
+    const size_t plane = (size_t)rows_total * kpad;
+    int *eo = (which ? eb_out : ex_out) + (size_t)z * rows_total + row;
+    if (r >= jb.R) {
+        for (int p = 0; p < oz::SLICES; ++p)
+            for (int k = lane * 4; k < kpad; k += 128) *(int *)(out + p * plane + k) = 0;
+        if (lane == 0) *eo = 0;
+        return;
+    }
+    const double *src = (which ? jb.Bg : jb.X) + z * jb.sx + (int64_t)r * jb.ld;
+    double mx = 0.0;
+    for (int k = lane; k < jb.K; k += 32) mx = fmax(mx, fabs(src[k]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    // e: 2^(e-1) <= max < 2^e, so |x| 2^-e < 1 and each slice digit |s| <= 127
+    const int e = mx > 0.0 ? ilogb(mx) + 1 : 0;
+    if (lane == 0) *eo = e;
+    for (int k0 = lane * 4; k0 < kpad; k0 += 128) {
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = k0 + q < jb.K ? scalbn(src[k0 + q], -e) : 0.0;
+#pragma unroll
+        for (int p = 0; p < oz::SLICES; ++p) {
+            uint32_t packed = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double t = v[q] * 128.0;       // exact (power of two)
+                const double d = trunc(t);           // |d| <= 127
+                v[q] = t - d;                        // exact: the remaining bits
+                packed |= ((uint32_t)(uint8_t)(int8_t)(int)d) << (8 * q);
+            }
+            *(uint32_t *)(out + p * plane + k0) = packed;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ the GEMM
+__global__ void __launch_bounds__(oz::THREADS, 1)
+    schur_oz_kernel(const __grid_constant__ CUtensorMap map_x,
+                    const __grid_constant__ CUtensorMap map_b, const OzJob *jobs,
+                    const int *tile_job, int rows_total, const int *ex_all, const int *eb_all,
+                    double *dense_out, int ld_out) {
+    using namespace oz;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t *full = (uint64_t *)(smem + NSTAGE * STAGE);
+    uint64_t *empty = full + NSTAGE;
+    uint64_t *tfull = empty + NSTAGE;
+    uint32_t *tmem_slot = (uint32_t *)(tfull + 1);
+    __shared__ int s_rseg[BM], s_roff[BM], s_cseg[BN], s_coff[BN], s_box[4];
+    constexpr int MAXT = 64;
+    __shared__ SchurTarget s_tbl[MAXT];
+    __shared__ int s_er[BM], s_ec[BN];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const OzJob jb = jobs[tile_job[blockIdx.x]];
+    const int z = blockIdx.y;
+    int I, J;
+    tri_tile_oz(blockIdx.x - jb.tile0, jb.R, I, J);
+    const int m0 = I * BM, n0 = J * BN;
+    const int nkb = (jb.K + BKB - 1) / BKB;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < NSTAGE; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tfull, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         su32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    // epilogue bookkeeping (row/column segments, exponents) while the pipeline runs
+    if (warp >= 2) {
+        const int t = threadIdx.x - 64;
+        for (int q = t; q < BM + BN; q += 32 * EPI_WARPS) {
+            const int x = q < BM ? m0 + q : n0 + (q - BM);
+            const int sg = x < jb.R ? jb.seg_of ? jb.seg_of[x] : 0 : -1;
+            const int off = sg >= 0 ? (jb.seg_of ? x - jb.seg_start[sg] : x) : 0;
+            if (q < BM) {
+                s_rseg[q] = sg;
+                s_roff[q] = off;
+                s_er[q] = ex_all[(size_t)z * rows_total + jb.row0 + x];
+            } else {
+                s_cseg[q - BM] = sg;
+                s_coff[q - BM] = off;
+                s_ec[q - BM] = eb_all[(size_t)z * rows_total + jb.row0 + x];
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % NSTAGE;
+                mbar_wait(&empty[s], ((kb / NSTAGE) & 1) ^ 1);
+                mbar_expect_tx(&full[s], STAGE);
+                unsigned char *a = smem + s * STAGE, *b = a + SLICES * A_SLICE;
+                for (int p = 0; p < SLICES; ++p) {
+                    tma_load_3d(a + p * A_SLICE, &map_x, &full[s], kb * BKB, jb.row0 + m0,
+                                z * SLICES + p);
+                    tma_load_3d(b + p * B_SLICE, &map_b, &full[s], kb * BKB, jb.row0 + n0,
+                                z * SLICES + p);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % NSTAGE;
+                mbar_wait(&full[s], (kb / NSTAGE) & 1);
+                tc_fence_after();
+                const uint32_t a = su32(smem + s * STAGE), b = a + SLICES * A_SLICE;
+#pragma unroll 1
+                for (int g = 0; g < SLICES; ++g)
+#pragma unroll 1
+                    for (int i = 0; i <= g; ++i)
+#pragma unroll
+                        for (int kk = 0; kk < 2; ++kk)
+                            mma_i8(tmem + g * BN, sdesc_sw64(a + i * A_SLICE + kk * 32),
+                                   sdesc_sw64(b + (g - i) * B_SLICE + kk * 32), IDESC,
+                                   (kb | i | kk) != 0);
+                tc_commit(&empty[s]);
+            }
+            tc_commit(tfull);
+        }
+    } else {
+        // ---------------------------------------------------------- epilogue
+        const int q = warp & 3, h = (warp - 2) >> 2;       // TMEM lane quadrant, column half
+        const int rl = q * 32 + lane;
+        mbar_wait(tfull, 0);
+        tc_fence_after();
+        double acc[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) acc[c] = 0.0;
+#pragma unroll 1
+        for (int g = SLICES - 1; g >= 0; --g) {
+            uint32_t v[32];
+            tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + g * BN + h * 32, v);
+            const double w = exp2(-7.0 * (g + 2));
+#pragma unroll
+            for (int c = 0; c < 32; ++c) acc[c] = fma((double)(int)v[c], w, acc[c]);
+        }
+        // stage the tile (scaled by the row exponent) in the freed pipeline buffers
+        double *ct = (double *)smem;
+        const double sr = exp2((double)s_er[rl]);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) ct[rl * CT_LD + h * 32 + c] = acc[c] * sr;
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
+        const int t = threadIdx.x - 64;
+        if (dense_out) {
+            // test path: dense C (rows_total x ld_out of the job) += X Bg^T tile, c >= r
+            for (int e = t; e < BM * BN; e += 32 * EPI_WARPS) {
+                const int r = e / BN, c = e % BN;
+                if (m0 + r < jb.R && n0 + c < jb.R && n0 + c >= m0 + r)
+                    dense_out[(size_t)z * jb.R * ld_out + (size_t)(m0 + r) * ld_out + n0 + c] =
+                        ct[r * CT_LD + c] * exp2((double)s_ec[c]);
+            }
+        } else {
+            if (t == 0) {
+                const int rlast = min(BM, jb.R - m0) - 1, clast = min(BN, jb.R - n0) - 1;
+                s_box[0] = s_rseg[0];
+                s_box[1] = s_rseg[rlast] - s_rseg[0] + 1;
+                s_box[2] = s_cseg[0];
+                s_box[3] = s_cseg[clast] - s_cseg[0] + 1;
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
+            const int alo = s_box[0], na = s_box[1], blo = s_box[2], nb = s_box[3];
+            const bool in_smem = na * nb <= MAXT;
+            if (in_smem)
+                for (int e = t; e < na * nb; e += 32 * EPI_WARPS)
+                    s_tbl[e] = jb.tbl[(size_t)(alo + e / nb) * jb.nseg + blo + e % nb];
+            asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
+            // warp w: rows w, w + 8, ...; lane: columns lane, lane + 32 (row-contiguous REDs)
+            const int ew = warp - 2;
+            for (int r = ew; r < BM; r += EPI_WARPS) {
+                const int gr = m0 + r, a = s_rseg[r], ra = s_roff[r];
+                if (a < 0) break;
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int cl = hh * 32 + lane, gc = n0 + cl;
+                    const int b = s_cseg[cl], cb = s_coff[cl];
+                    if (b < 0 || gc < gr) continue;
+                    const SchurTarget e = in_smem ? s_tbl[(a - alo) * nb + (b - blo)]
+                                                  : jb.tbl[(size_t)a * jb.nseg + b];
+                    if (!e.base) continue;
+                    const double val = ct[r * CT_LD + cl] * exp2((double)s_ec[cl]);
+                    double *base = e.base + z * e.bs;
+                    red_add_f64(base + (e.trans ? (int64_t)cb * e.ldc + ra : (int64_t)ra * e.ldc + cb),
+                                -val);
+                    if (a == b && cb != ra) red_add_f64(base + (int64_t)cb * e.ldc + ra, -val);
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
+// ------------------------------------------------------------------- host side
+namespace {
+typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiled encode_fn() {
+    static EncodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiled)p;
+    });
+    return fn;
+}
+cudaError_t make_map(CUtensorMap *m, const int8_t *base, int kpad, int rows, int planes,
+                     int box_rows) {
+    EncodeTiled fn = encode_fn();
+    if (!fn) return cudaErrorNotSupported;
+    cuuint64_t dims[3] = {(cuuint64_t)kpad, (cuuint64_t)rows, (cuuint64_t)planes};
+    cuuint64_t strides[2] = {(cuuint64_t)kpad, (cuuint64_t)kpad * rows};
+    cuuint32_t box[3] = {(cuuint32_t)oz::BKB, (cuuint32_t)box_rows, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void *)base, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+}  // namespace
+
+size_t schur_oz_scratch_bytes(int rows_total, int kpad, int nshift) {
+    const size_t sl = (size_t)oz::SLICES * rows_total * kpad * nshift;
+    const size_t ex = (size_t)rows_total * nshift * sizeof(int);
+    return 2 * sl + 2 * ((ex + 255) / 256 * 256);
+}
+
+// jobs / row_job / tile_job are device arrays (row_job: one entry per 128 packed rows);
+// scratch holds schur_oz_scratch_bytes(rows_total, kpad, nshift) bytes.
+cudaError_t launch_schur_oz(const OzJob *jobs, const int *row_job, const int *tile_job,
+                            int rows_total, int kpad, int total_tiles, int nshift, void *scratch,
+                            cudaStream_t st, double *dense_out, int ld_out) {
+    if (total_tiles <= 0 || nshift <= 0 || rows_total <= 0) return cudaSuccess;
+    if (kpad % oz::BKB || rows_total % oz::BM) return cudaErrorInvalidValue;
+    const size_t sl = (size_t)oz::SLICES * rows_total * kpad * nshift;
+    const size_t ex = ((size_t)rows_total * nshift * sizeof(int) + 255) / 256 * 256;
+    int8_t *sx = (int8_t *)scratch, *sb = sx + sl;
+    int *exr = (int *)(sb + sl), *ebr = (int *)((char *)exr + ex);
+    dim3 g1((rows_total + 7) / 8, nshift, 2);
+    oz_split_kernel<<<g1, 256, 0, st>>>(jobs, row_job, rows_total, kpad, sx, sb, exr, ebr);
+    CUtensorMap mx, mb;
+    cudaError_t e = make_map(&mx, sx, kpad, rows_total, oz::SLICES * nshift, oz::BM);
+    if (e != cudaSuccess) return e;
+    e = make_map(&mb, sb, kpad, rows_total, oz::SLICES * nshift, oz::BN);
+    if (e != cudaSuccess) return e;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaFuncSetAttribute(schur_oz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, oz::SMEM);
+    });
+    dim3 g2(total_tiles, nshift);
+    schur_oz_kernel<<<g2, oz::THREADS, oz::SMEM, st>>>(mx, mb, jobs, tile_job, rows_total, exr, ebr,
+                                                        dense_out, ld_out);
+    return cudaGetLastError();
+}
+
+}  // namespace h2l

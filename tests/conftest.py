@@ -7,7 +7,9 @@ import glob
 import os
 import sys
 
-import numpy as np
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"))
+import pin_host_fp  # noqa: E402,F401  (before numpy: payloads rebuilt here round like the reference's)
+import numpy as np  # noqa: E402
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

@@ -28,7 +28,8 @@ import subprocess
 import sys
 import tempfile
 
-import numpy as np
+import pin_host_fp  # noqa: F401  (before numpy: host-independent rounding, see its docstring)
+import numpy as np  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(os.path.dirname(HERE))
@@ -168,7 +169,8 @@ def _ref_config_H(name, n, leaf):
     rcloud = PointCloud(cloud.coords)
     rtree = rbuild(rcloud, leaf)
     rst = rclassify(rtree, strong(1.0))
-    return construct(kern, rtree, rst, configs.CONFIGS[name].eps)
+    with pin_host_fp.single_thread():
+        return construct(kern, rtree, rst, configs.CONFIGS[name].eps)
 
 
 def _record(name, H, nshift=40, seed=0):
@@ -293,6 +295,7 @@ def gen_prod(only=()):
             continue
         t0 = time.perf_counter()
         cfg = configs.CONFIGS[cfgname]
+        assert not pin_host_fp.check(), pin_host_fp.check()
         H = _ref_config_H(cfgname, n, leaf)
         t_con = time.perf_counter() - t0
         digest = payload_digest(H)

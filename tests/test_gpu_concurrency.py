@@ -63,7 +63,7 @@ def test_bk_bit_exact_under_load(n, count):
 
 
 def test_gemm_matches_naive_under_load():
-    lib = _native.load_library()
+    lib = _native.load_testing_library()
     f = lib.h2l_internal_gemm_check
     f.argtypes = [ctypes.c_int] * 7 + [ctypes.POINTER(ctypes.c_double)]
     md = ctypes.c_double()

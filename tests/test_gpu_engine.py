@@ -213,7 +213,7 @@ def test_cluster_bk_bit_identical_to_single_cta(n):
     kernel's arithmetic: factor, permutation, pivot blocks and counts bit-identical."""
     import ctypes
 
-    lib = _native.load_library()
+    lib = _native.load_testing_library()
     f = lib.h2l_internal_bk_engine
     f.restype = ctypes.c_int
     rng = np.random.default_rng(n)
@@ -252,7 +252,7 @@ def test_gram_ordering_cluster_qr(n):
 
     import scipy.linalg
 
-    lib = _native.load_library()
+    lib = _native.load_testing_library()
     f = lib.h2l_internal_gram_order
     f.restype = ctypes.c_int
     rng = np.random.default_rng(n)

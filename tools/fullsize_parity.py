@@ -20,7 +20,10 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-SHIFTS = {"cfg2": [-10.0], "cfg3": [None], "cfg4": [None], "cfg5": [None, -0.5]}
+# candidate shifts as fractions of the Gershgorin interval (plus config 2's mu = -10 of the
+# survey); each is certified >= DELTA from the spectrum by equal counts at mu -/+ DELTA
+SHIFTS = {"cfg2": [-10.0, 0.37], "cfg3": [0.5, 0.41], "cfg4": [0.5], "cfg5": [0.5, 0.47]}
+GUARD = 100.0  # DELTA = GUARD * eps * max(|lo|, |hi|) of the interval
 PROD = {"cfg2": (7, 1, 1, 0), "cfg3": (8, 2, 2, 0), "cfg4": (2, 1, 2, 1), "cfg5": (8, 2, 2, 0)}
 
 
@@ -47,15 +50,28 @@ def main():
         torch.cuda.synchronize()
         t_con = time.perf_counter() - t0
         iv = gpu_build.gershgorin_device(H._kernel)
-        mus = [0.5 * (iv[0] + iv[1]) if m is None else m for m in SHIFTS[name]]
+        cands = [m if m < 0 else iv[0] + m * (iv[1] - iv[0]) for m in SHIFTS[name]]
         eng = _native.engine_for(H, 0)
+        # certify each candidate: equal negative counts at mu - delta, mu, mu + delta means no
+        # eigenvalue of the factored matrix within delta (the parity criterion's guard band)
+        delta = GUARD * H.eps * max(abs(iv[0]), abs(iv[1]))
+        eng.set_option("max_batch", 8)
+        probe = [x for m in cands for x in (m - delta, m, m + delta)]
+        pc, _, _ = ldl_counts_array(H, probe)
+        mus, rejected = [], []
+        for q, m in enumerate(cands):
+            negs = [int(pc[3 * q + d, 0]) for d in range(3)]
+            (mus if len(set(negs)) == 1 else rejected).append(m)
+            print(name, "candidate", m, "negatives at -d/0/+d", negs, flush=True)
         gpu = {}
-        for label, (mb, conc, sched, order) in (("reference_order", (4, 1, 0, 1 if name == "cfg4" else 0)),
-                                                 ("production", PROD[name])):
+        for label, (mb, conc, sched, order, budget) in (
+                ("reference_order", (4, 1, 0, 1 if name == "cfg4" else 0, 0)),
+                ("production", PROD[name] + (1,))):
             eng.set_option("max_batch", mb)
             eng.set_option("concurrency", conc)
             eng.set_option("schedule", sched)
             eng.set_option("elim_order", order)
+            eng.set_option("qr_budget", budget)
             counts, status, st = ldl_counts_array(H, mus)
             gpu[label] = {"counts": counts.tolist(), "status": status.tolist(),
                           "ms_total": st["ms_total"], "rank_added": st["rank_added"],
@@ -92,6 +108,7 @@ def main():
         except Exception:  # noqa: BLE001
             threads = os.cpu_count()
         rec = {"config": name, "n": cloud.n, "interval": list(iv), "mus": mus,
+               "guard_delta": delta, "rejected_candidates": rejected,
                "construct_device_s": t_con, "export_s": t_exp, "gpu": gpu, "oracle": cpu,
                "host_threads": threads, "cpu_count": os.cpu_count(),
                "counts_equal": all(

@@ -10,7 +10,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2311_08618_b200 import _native  # noqa: E402
 
-lib = _native.load_library()
+lib = _native.load_testing_library()
 f = lib.h2l_internal_gemm_bench
 f.argtypes = [ctypes.c_int] * 8 + [ctypes.POINTER(ctypes.c_double)] * 2
 f.restype = ctypes.c_int

@@ -2,7 +2,7 @@
 import ctypes, os, sys, threading
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2311_08618_b200 import _native
-lib = _native.load_library()
+lib = _native.load_testing_library()
 f = lib.h2l_internal_gemm_check
 f.argtypes = [ctypes.c_int] * 7 + [ctypes.POINTER(ctypes.c_double)]
 f.restype = ctypes.c_int
