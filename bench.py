@@ -309,6 +309,8 @@ def run_ours(args):
     wl.config["waves"] = f"{conc} concurrent wave(s) of <= {(S + conc - 1) // conc} shifts"
     sched = args.schedule if args.schedule >= 0 else (1 if wl.name in ("cfg1", "cfg2") else 2)
     eng.set_option("schedule", sched)
+    if args.schur_arith >= 0:
+        eng.set_option("schur_arith", args.schur_arith)
     wl.config["schedule"] = {0: "one cluster at a time, ascending (the reference)",
                              1: "ascending-order wavefronts (level-batched, reference order)",
                              2: "colour classes (level-batched, re-ordered)"}[sched]
@@ -670,6 +672,8 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--schedule", type=int, default=-1, help="elimination schedule (engine option)")
+    ap.add_argument("--schur-arith", type=int, default=-1,
+                    help="Schur update arithmetic (engine option schur_arith): 0 DMMA, 1 INT8 Ozaki")
     ap.add_argument("--no-batch32", action="store_true", help="skip config 2's 32-shift call")
     args = ap.parse_args()
     if args.impl == "reference":

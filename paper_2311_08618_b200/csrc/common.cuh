@@ -187,7 +187,7 @@ int schur_oz_tiles(int R);
 size_t schur_oz_scratch_bytes(int rows_total, int kpad, int nshift);
 cudaError_t launch_schur_oz(const OzJob *jobs, const int *row_job, const int *tile_job,
                             int rows_total, int kpad, int total_tiles, int nshift, void *scratch,
-                            cudaStream_t st, double *dense_out = nullptr, int ld_out = 0);
+                            cudaStream_t st, double *dense_out = nullptr, int ld_out = 0, int probe = 0);
 void launch_schur_sym(const double *X, const double *Bg, int64_t sx, int ld, int R, int K,
                       const int *seg_of, const int *seg_start, int nseg, const SchurTarget *tbl,
                       int nshift, cudaStream_t st, int variant = 0);

@@ -33,97 +33,38 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "tcgen05.cuh"
 
 namespace h2l {
 
 namespace oz {
+using namespace tc;
 
 constexpr int SLICES = 8;
-constexpr int BM = 128, BN = 64, BKB = 64;           // tile rows, tile cols, K bytes per stage
-constexpr int A_SLICE = BM * BKB, B_SLICE = BN * BKB;  // 8 KB, 4 KB
-constexpr int STAGE = SLICES * (A_SLICE + B_SLICE);    // 96 KB
-constexpr int NSTAGE = 2;
+constexpr int BM = 128, BN = 64, BKB = 32;           // tile rows, tile cols, K bytes per stage
+constexpr int A_SLICE = BM * BKB, B_SLICE = BN * BKB;  // 4 KB, 2 KB
+constexpr int STAGE = SLICES * (A_SLICE + B_SLICE);    // 48 KB
+constexpr int NSTAGE = 3;
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 64 + 32 * EPI_WARPS;           // 320
 constexpr int CT_LD = BN + 1;                          // staged tile row stride (doubles)
-constexpr int SMEM = NSTAGE * STAGE + 1024 /*align*/ + 256 /*barriers*/;
-static_assert(BM * CT_LD * 8 <= NSTAGE * STAGE, "staged tile fits the pipeline buffers");
+constexpr int CT_BYTES = BM * CT_LD * 8;
+constexpr int SMEM = NSTAGE * STAGE + CT_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
-__device__ __forceinline__ uint32_t su32(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t n) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@P1 bra DONE_%=;\n\t"
-        "bra WAIT_%=;\n"
-        "DONE_%=:\n\t}" ::"r"(su32(b)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0,
-                                            int c1, int c2) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(su32(dst)),
-        "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
-        : "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_commit(uint64_t *bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                     su32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
-                                       uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc)
-        : "memory");
-}
-// K-major operand tile with 64-byte swizzle: rows of 64 bytes, 8-row groups 512 B apart
-__device__ __forceinline__ uint64_t sdesc_sw64(uint32_t saddr) {
+// K-major operand tile with 32-byte swizzle: rows of 32 bytes (one K step), 8-row
+// groups 256 B apart
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address
     d |= (uint64_t)1 << 16;                          // leading byte offset (unused: swizzled K-major)
-    d |= (uint64_t)(512 >> 4) << 32;                 // stride byte offset: next 8-row group
+    d |= (uint64_t)(8 * BKB >> 4) << 32;             // stride byte offset: next 8-row group
     d |= (uint64_t)1 << 46;                          // descriptor version (sm_100)
-    d |= (uint64_t)4 << 61;                          // SWIZZLE_64B
+    d |= (uint64_t)6 << 61;                          // SWIZZLE_32B
     return d;
 }
-// instruction descriptor: kind::i8, s32 accumulate, signed A/B, both K-major, M=128, N=64
-constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
-
-__device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&v)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
-          "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
-          "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-        : "r"(addr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+// instruction descriptor: kind::i8, s32 accumulate, signed A/B, both K-major, M=128, N=n
+__host__ __device__ constexpr uint32_t idesc_n(int n) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
 // tile t of a job with R rows -> (I, J): row tile I (128), column tile J (64), J >= 2I
@@ -200,30 +141,41 @@ __global__ void __launch_bounds__(256) oz_split_kernel(const OzJob *jobs, const 
 }
 
 // ------------------------------------------------------------------ the GEMM
+// exact int32 -> fp64 without the XU pipe: the bits of 2^52 + 2^51 + v, minus 2^52 + 2^51
+__device__ __forceinline__ double i2d_exact(int v) {
+    return __hiloint2double(0x43380000 + (v >> 31), v) - 6755399441055744.0;
+}
+// 2^e (exact; fast path for the normal range)
+__device__ __forceinline__ double pow2i(int e) {
+    return (e >= -1022 && e <= 1023) ? __longlong_as_double((long long)(e + 1023) << 52)
+                                     : scalbn(1.0, e);
+}
+
+// Persistent: one CTA per SM walks the (shift, tile) items; the TMA producer and the
+// MMA issuer run ahead across items, the epilogue of item i overlaps the MMAs of
+// item i + 1 (it releases tensor memory right after reading the 8 group totals).
 __global__ void __launch_bounds__(oz::THREADS, 1)
     schur_oz_kernel(const __grid_constant__ CUtensorMap map_x,
                     const __grid_constant__ CUtensorMap map_b, const OzJob *jobs,
-                    const int *tile_job, int rows_total, const int *ex_all, const int *eb_all,
-                    double *dense_out, int ld_out) {
+                    const int *tile_job, int total_tiles, int nshift, int rows_total,
+                    const int *ex_all, const int *eb_all, double *dense_out, int ld_out,
+                    int probe) {
     using namespace oz;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t *full = (uint64_t *)(smem + NSTAGE * STAGE);
+    double *ct = (double *)(smem + NSTAGE * STAGE);           // staged output tile
+    uint64_t *full = (uint64_t *)(smem + NSTAGE * STAGE + CT_BYTES);
     uint64_t *empty = full + NSTAGE;
     uint64_t *tfull = empty + NSTAGE;
-    uint32_t *tmem_slot = (uint32_t *)(tfull + 1);
+    uint64_t *tempty = tfull + 1;
+    uint32_t *tmem_slot = (uint32_t *)(tempty + 1);
     __shared__ int s_rseg[BM], s_roff[BM], s_cseg[BN], s_coff[BN], s_box[4];
     constexpr int MAXT = 64;
     __shared__ SchurTarget s_tbl[MAXT];
-    __shared__ int s_er[BM], s_ec[BN];
+    __shared__ double s_sr[BM], s_sc[BN];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const OzJob jb = jobs[tile_job[blockIdx.x]];
-    const int z = blockIdx.y;
-    int I, J;
-    tri_tile_oz(blockIdx.x - jb.tile0, jb.R, I, J);
-    const int m0 = I * BM, n0 = J * BN;
-    const int nkb = (jb.K + BKB - 1) / BKB;
+    const int items = total_tiles * nshift;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < NSTAGE; ++s) {
@@ -231,6 +183,7 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
             mbar_init(&empty[s], 1);
         }
         mbar_init(tfull, 1);
+        mbar_init(tempty, EPI_WARPS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
@@ -241,98 +194,130 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
-    // epilogue bookkeeping (row/column segments, exponents) while the pipeline runs
-    if (warp >= 2) {
-        const int t = threadIdx.x - 64;
-        for (int q = t; q < BM + BN; q += 32 * EPI_WARPS) {
-            const int x = q < BM ? m0 + q : n0 + (q - BM);
-            const int sg = x < jb.R ? jb.seg_of ? jb.seg_of[x] : 0 : -1;
-            const int off = sg >= 0 ? (jb.seg_of ? x - jb.seg_start[sg] : x) : 0;
-            if (q < BM) {
-                s_rseg[q] = sg;
-                s_roff[q] = off;
-                s_er[q] = ex_all[(size_t)z * rows_total + jb.row0 + x];
-            } else {
-                s_cseg[q - BM] = sg;
-                s_coff[q - BM] = off;
-                s_ec[q - BM] = eb_all[(size_t)z * rows_total + jb.row0 + x];
-            }
-        }
-    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    auto locate = [&](int item, OzJob &jb, int &z, int &m0, int &n0) {
+        z = item / total_tiles;
+        const int t = item - z * total_tiles;
+        jb = jobs[tile_job[t]];
+        int I, J;
+        tri_tile_oz(t - jb.tile0, jb.R, I, J);
+        m0 = I * BM;
+        n0 = J * BN;
+    };
+
     if (warp == 0) {
         if (lane == 0) {
-            for (int kb = 0; kb < nkb; ++kb) {
-                const int s = kb % NSTAGE;
-                mbar_wait(&empty[s], ((kb / NSTAGE) & 1) ^ 1);
-                mbar_expect_tx(&full[s], STAGE);
-                unsigned char *a = smem + s * STAGE, *b = a + SLICES * A_SLICE;
-                for (int p = 0; p < SLICES; ++p) {
-                    tma_load_3d(a + p * A_SLICE, &map_x, &full[s], kb * BKB, jb.row0 + m0,
-                                z * SLICES + p);
-                    tma_load_3d(b + p * B_SLICE, &map_b, &full[s], kb * BKB, jb.row0 + n0,
-                                z * SLICES + p);
+            int kstep = 0;
+            for (int item = blockIdx.x; item < items; item += gridDim.x) {
+                OzJob jb;
+                int z, m0, n0;
+                locate(item, jb, z, m0, n0);
+                const int nkb = (jb.K + BKB - 1) / BKB;
+                for (int kb = 0; kb < nkb; ++kb, ++kstep) {
+                    const int s = kstep % NSTAGE;
+                    mbar_wait(&empty[s], ((kstep / NSTAGE) & 1) ^ 1);
+                    mbar_expect_tx(&full[s], STAGE);
+                    unsigned char *a = smem + s * STAGE, *b = a + SLICES * A_SLICE;
+                    for (int p = 0; p < SLICES; ++p) {
+                        tma_load_3d(a + p * A_SLICE, &map_x, &full[s], kb * BKB, jb.row0 + m0,
+                                    z * SLICES + p);
+                        tma_load_3d(b + p * B_SLICE, &map_b, &full[s], kb * BKB, jb.row0 + n0,
+                                    z * SLICES + p);
+                    }
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            for (int kb = 0; kb < nkb; ++kb) {
-                const int s = kb % NSTAGE;
-                mbar_wait(&full[s], (kb / NSTAGE) & 1);
+            int kstep = 0, it = 0;
+            for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+                OzJob jb;
+                int z, m0, n0;
+                locate(item, jb, z, m0, n0);
+                const int nkb = (jb.K + BKB - 1) / BKB;
+                mbar_wait(tempty, (it & 1) ^ 1);     // the epilogue has read the previous totals
                 tc_fence_after();
-                const uint32_t a = su32(smem + s * STAGE), b = a + SLICES * A_SLICE;
-#pragma unroll 1
-                for (int g = 0; g < SLICES; ++g)
-#pragma unroll 1
-                    for (int i = 0; i <= g; ++i)
+                for (int kb = 0; kb < nkb; ++kb, ++kstep) {
+                    const int s = kstep % NSTAGE;
+                    // probe (benchmarking only): 1 = MMAs without waiting for the loads,
+                    // 2 = loads without MMAs
+                    if (probe != 1) mbar_wait(&full[s], (kstep / NSTAGE) & 1);
+                    tc_fence_after();
+                    if (probe == 2) {
+                        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[s])) : "memory");
+                        continue;
+                    }
+                    const uint32_t a = su32(smem + s * STAGE), b = a + SLICES * A_SLICE;
+                    // slice i of X against the stacked slices [T_0; T_1; ...; T_{7-i}] of
+                    // Bg (contiguous in shared memory): one wide MMA lands every pair
+                    // (i, j) in the accumulator of its group g = i + j (columns g * 64).
+                    // An MMA costs the same for any N <= 256, so 12 wide instructions
+                    // per K step replace 36 of N = 64.
 #pragma unroll
-                        for (int kk = 0; kk < 2; ++kk)
-                            mma_i8(tmem + g * BN, sdesc_sw64(a + i * A_SLICE + kk * 32),
-                                   sdesc_sw64(b + (g - i) * B_SLICE + kk * 32), IDESC,
-                                   (kb | i | kk) != 0);
-                tc_commit(&empty[s]);
+                    for (int i = 0; i < SLICES; ++i) {
+                        const int cols = (SLICES - i) * BN;
+#pragma unroll
+                        for (int off = 0; off < cols; off += 256) {
+                            const int n = cols - off < 256 ? cols - off : 256;
+                            mma_i8(tmem + i * BN + off, sdesc(a + i * A_SLICE),
+                                   sdesc(b + (off / BN) * B_SLICE), idesc_n(n), (kb | i) != 0);
+                        }
+                    }
+                    tc_commit(&empty[s]);
+                }
+                tc_commit(tfull);
             }
-            tc_commit(tfull);
         }
     } else {
         // ---------------------------------------------------------- epilogue
         const int q = warp & 3, h = (warp - 2) >> 2;       // TMEM lane quadrant, column half
-        const int rl = q * 32 + lane;
-        mbar_wait(tfull, 0);
-        tc_fence_after();
-        double acc[32];
-#pragma unroll
-        for (int c = 0; c < 32; ++c) acc[c] = 0.0;
-#pragma unroll 1
-        for (int g = SLICES - 1; g >= 0; --g) {
-            uint32_t v[32];
-            tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + g * BN + h * 32, v);
-            const double w = exp2(-7.0 * (g + 2));
-#pragma unroll
-            for (int c = 0; c < 32; ++c) acc[c] = fma((double)(int)v[c], w, acc[c]);
-        }
-        // stage the tile (scaled by the row exponent) in the freed pipeline buffers
-        double *ct = (double *)smem;
-        const double sr = exp2((double)s_er[rl]);
-#pragma unroll
-        for (int c = 0; c < 32; ++c) ct[rl * CT_LD + h * 32 + c] = acc[c] * sr;
-        asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
-        const int t = threadIdx.x - 64;
-        if (dense_out) {
-            // test path: dense C (rows_total x ld_out of the job) += X Bg^T tile, c >= r
-            for (int e = t; e < BM * BN; e += 32 * EPI_WARPS) {
-                const int r = e / BN, c = e % BN;
-                if (m0 + r < jb.R && n0 + c < jb.R && n0 + c >= m0 + r)
-                    dense_out[(size_t)z * jb.R * ld_out + (size_t)(m0 + r) * ld_out + n0 + c] =
-                        ct[r * CT_LD + c] * exp2((double)s_ec[c]);
+        const int rl = q * 32 + lane, t = threadIdx.x - 64, ew = warp - 2;
+        int it = 0;
+        for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+            OzJob jb;
+            int z, m0, n0;
+            locate(item, jb, z, m0, n0);
+            // the previous item's scatter is done with the staged tile and tables
+            asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
+            for (int x = t; x < BM + BN; x += 32 * EPI_WARPS) {
+                const int g = x < BM ? m0 + x : n0 + (x - BM);
+                const int sg = g < jb.R ? (jb.seg_of ? jb.seg_of[g] : 0) : -1;
+                const int off = sg >= 0 ? (jb.seg_of ? g - jb.seg_start[sg] : g) : 0;
+                if (x < BM) {
+                    s_rseg[x] = sg;
+                    s_roff[x] = off;
+                    s_sr[x] = pow2i(ex_all[(size_t)z * rows_total + jb.row0 + g]);
+                } else {
+                    s_cseg[x - BM] = sg;
+                    s_coff[x - BM] = off;
+                    s_sc[x - BM] = pow2i(eb_all[(size_t)z * rows_total + jb.row0 + g]);
+                }
             }
-        } else {
-            if (t == 0) {
+            mbar_wait(tfull, it & 1);
+            tc_fence_after();
+            double acc[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) acc[c] = 0.0;
+#pragma unroll 1
+            for (int g = SLICES - 1; g >= 0; --g) {
+                uint32_t v[32];
+                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + g * BN + h * 32, v);
+                const double w = pow2i(-7 * (g + 2));
+#pragma unroll
+                for (int c = 0; c < 32; ++c) acc[c] = fma(i2d_exact((int)v[c]), w, acc[c]);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(tempty)) : "memory");
+            asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");  // tables ready
+            const double sr = s_sr[rl];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) ct[rl * CT_LD + h * 32 + c] = acc[c] * sr;
+            if (t == 0 && !dense_out) {
                 const int rlast = min(BM, jb.R - m0) - 1, clast = min(BN, jb.R - n0) - 1;
                 s_box[0] = s_rseg[0];
                 s_box[1] = s_rseg[rlast] - s_rseg[0] + 1;
@@ -340,6 +325,16 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
                 s_box[3] = s_cseg[clast] - s_cseg[0] + 1;
             }
             asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
+            if (dense_out) {
+                // test path: dense C (R x ld_out per shift) = X Bg^T on the upper triangle
+                for (int e = t; e < BM * BN; e += 32 * EPI_WARPS) {
+                    const int r = e / BN, c = e % BN;
+                    if (m0 + r < jb.R && n0 + c < jb.R && n0 + c >= m0 + r)
+                        dense_out[(size_t)z * jb.R * ld_out + (size_t)(m0 + r) * ld_out + n0 + c] =
+                            ct[r * CT_LD + c] * s_sc[c];
+                }
+                continue;
+            }
             const int alo = s_box[0], na = s_box[1], blo = s_box[2], nb = s_box[3];
             const bool in_smem = na * nb <= MAXT;
             if (in_smem)
@@ -347,7 +342,6 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
                     s_tbl[e] = jb.tbl[(size_t)(alo + e / nb) * jb.nseg + blo + e % nb];
             asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
             // warp w: rows w, w + 8, ...; lane: columns lane, lane + 32 (row-contiguous REDs)
-            const int ew = warp - 2;
             for (int r = ew; r < BM; r += EPI_WARPS) {
                 const int gr = m0 + r, a = s_rseg[r], ra = s_roff[r];
                 if (a < 0) break;
@@ -359,7 +353,7 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
                     const SchurTarget e = in_smem ? s_tbl[(a - alo) * nb + (b - blo)]
                                                   : jb.tbl[(size_t)a * jb.nseg + b];
                     if (!e.base) continue;
-                    const double val = ct[r * CT_LD + cl] * exp2((double)s_ec[cl]);
+                    const double val = ct[r * CT_LD + cl] * s_sc[cl];
                     double *base = e.base + z * e.bs;
                     red_add_f64(base + (e.trans ? (int64_t)cb * e.ldc + ra : (int64_t)ra * e.ldc + cb),
                                 -val);
@@ -404,7 +398,7 @@ cudaError_t make_map(CUtensorMap *m, const int8_t *base, int kpad, int rows, int
     cuuint32_t box[3] = {(cuuint32_t)oz::BKB, (cuuint32_t)box_rows, 1};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void *)base, dims, strides, box, es,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
@@ -420,9 +414,9 @@ size_t schur_oz_scratch_bytes(int rows_total, int kpad, int nshift) {
 // scratch holds schur_oz_scratch_bytes(rows_total, kpad, nshift) bytes.
 cudaError_t launch_schur_oz(const OzJob *jobs, const int *row_job, const int *tile_job,
                             int rows_total, int kpad, int total_tiles, int nshift, void *scratch,
-                            cudaStream_t st, double *dense_out, int ld_out) {
+                            cudaStream_t st, double *dense_out, int ld_out, int probe) {
     if (total_tiles <= 0 || nshift <= 0 || rows_total <= 0) return cudaSuccess;
-    if (kpad % oz::BKB || rows_total % oz::BM) return cudaErrorInvalidValue;
+    if (kpad % 64 || rows_total % oz::BM) return cudaErrorInvalidValue;
     const size_t sl = (size_t)oz::SLICES * rows_total * kpad * nshift;
     const size_t ex = ((size_t)rows_total * nshift * sizeof(int) + 255) / 256 * 256;
     int8_t *sx = (int8_t *)scratch, *sb = sx + sl;
@@ -438,9 +432,15 @@ cudaError_t launch_schur_oz(const OzJob *jobs, const int *row_job, const int *ti
     std::call_once(once, [] {
         cudaFuncSetAttribute(schur_oz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, oz::SMEM);
     });
-    dim3 g2(total_tiles, nshift);
-    schur_oz_kernel<<<g2, oz::THREADS, oz::SMEM, st>>>(mx, mb, jobs, tile_job, rows_total, exr, ebr,
-                                                        dense_out, ld_out);
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int items = total_tiles * nshift;
+    schur_oz_kernel<<<items < nsm ? items : nsm, oz::THREADS, oz::SMEM, st>>>(
+        mx, mb, jobs, tile_job, total_tiles, nshift, rows_total, exr, ebr, dense_out, ld_out, probe);
     return cudaGetLastError();
 }
 

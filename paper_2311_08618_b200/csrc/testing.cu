@@ -293,7 +293,8 @@ extern "C" int h2l_internal_gemm_check(int device, int M, int N, int K, int ntas
 // triangle (c >= r; C is R x R, host, lower triangle left untouched).  reps > 0
 // times `reps` launches (split + GEMM) and returns the mean in *ms_out.
 extern "C" int h2l_internal_schur_oz(int device, int R, int K, int nshift, const double *X,
-                                     const double *Bg, double *C, int reps, double *ms_out) {
+                                     const double *Bg, double *C, int reps, double *ms_out,
+                                     int probe) {
     return guarded(nullptr, [&] {
         CK(cudaSetDevice(device));
         const int64_t rk = (int64_t)R * K, rr = (int64_t)R * R;
@@ -327,7 +328,8 @@ extern "C" int h2l_internal_schur_oz(int device, int R, int K, int nshift, const
             CK(cudaEventCreate(&e1));
             CK(cudaEventRecord(e0));
             for (int q = 0; q < reps; ++q)
-                CK(h2l::launch_schur_oz(djob, drj, dtj, rpad, kpad, tiles, nshift, scratch, 0, dc, R));
+                CK(h2l::launch_schur_oz(djob, drj, dtj, rpad, kpad, tiles, nshift, scratch, 0, dc, R,
+                                        probe));
             CK(cudaEventRecord(e1));
             CK(cudaEventSynchronize(e1));
             float ms = 0.f;
@@ -338,5 +340,81 @@ extern "C" int h2l_internal_schur_oz(int device, int R, int K, int nshift, const
         }
         cudaFree(dx); cudaFree(db); cudaFree(dc); cudaFree(djob); cudaFree(drj); cudaFree(dtj);
         cudaFree(scratch);
+    });
+}
+
+// ---- tcgen05 INT8 MMA issue-rate probe: one CTA per SM issues `count` MMAs of shape
+// M=128 x N=n x K=32 (SWIZZLE_32B K-major operands, zeroed shared memory) from one
+// thread and reports cycles per MMA.  order 0: runs of 8 MMAs into the same
+// accumulator; 1: consecutive MMAs rotate over accumulators.
+#include "tcgen05.cuh"
+namespace h2l {
+__global__ void umma_rate_kernel(int n, int order, int count, long long *cycles) {
+    using namespace tc;
+    extern __shared__ __align__(1024) unsigned char sm_raw[];
+    unsigned char *sm = (unsigned char *)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
+    __shared__ uint32_t slot;
+    __shared__ __align__(8) uint64_t bar;
+    for (int q = threadIdx.x; q < 96 * 1024 / 16; q += blockDim.x) ((int4 *)sm)[q] = make_int4(0, 0, 0, 0);
+    if (threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&slot)) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = slot;
+    if (threadIdx.x == 0) {
+        auto sdesc32 = [](uint32_t a) {
+            uint64_t d = (uint64_t)((a >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)16 << 32) |
+                         ((uint64_t)1 << 46) | ((uint64_t)6 << 61);
+            return d;
+        };
+        const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) |
+                               ((uint32_t)(128 >> 4) << 24);
+        const int nacc = 512 / n;
+        const uint32_t a0 = su32(sm), b0 = a0 + 8 * 4096;
+        const long long t0 = clock64();
+        for (int c = 0; c < count; ++c) {
+            const int g = order == 0 ? (c / 8) % nacc : c % nacc;
+            mma_i8(tmem + g * n, sdesc32(a0 + (c & 7) * 4096), sdesc32(b0 + (c & 7) * (n * 32)), idesc, 1);
+        }
+        tc_commit(&bar);
+        mbar_wait(&bar, 0);
+        cycles[blockIdx.x] = clock64() - t0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+}  // namespace h2l
+
+extern "C" int h2l_internal_umma_rate(int device, int n, int order, int count, double *cyc_per_mma) {
+    return guarded(nullptr, [&] {
+        CK(cudaSetDevice(device));
+        int nsm = 0;
+        CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+        long long *d;
+        CK(cudaMalloc(&d, sizeof(long long) * nsm));
+        const int smem = 96 * 1024 + 1024 + 8 * 256 * 32;
+        CK(cudaFuncSetAttribute(h2l::umma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        h2l::umma_rate_kernel<<<nsm, 128, 200 * 1024>>>(n, order, count, d);
+        (void)smem;
+        CK(cudaGetLastError());
+        CK(cudaDeviceSynchronize());
+        std::vector<long long> h(nsm);
+        CK(cudaMemcpy(h.data(), d, sizeof(long long) * nsm, cudaMemcpyDeviceToHost));
+        double mx = 0;
+        for (auto v : h) mx = std::max(mx, (double)v);
+        *cyc_per_mma = mx / count;
+        cudaFree(d);
     });
 }

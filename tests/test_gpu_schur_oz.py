@@ -25,14 +25,14 @@ def _oz(X, B, reps=0):
     lib = _native.load_testing_library()
     f = lib.h2l_internal_schur_oz
     f.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _f64p, _f64p, _f64p,
-                  ctypes.c_int, _f64p]
+                  ctypes.c_int, _f64p, ctypes.c_int]
     s, R, K = X.shape
     X = np.ascontiguousarray(X)
     B = np.ascontiguousarray(B)
     C = np.zeros((s, R, R))
     ms = ctypes.c_double(0.0)
     rc = f(0, R, K, s, X.ctypes.data_as(_f64p), B.ctypes.data_as(_f64p), C.ctypes.data_as(_f64p),
-           reps, ctypes.byref(ms))
+           reps, ctypes.byref(ms), 0)
     assert rc == 0, lib.h2l_testing_last_error().decode()
     return C, ms.value
 

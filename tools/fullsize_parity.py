@@ -20,10 +20,13 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-# candidate shifts as fractions of the Gershgorin interval (plus config 2's mu = -10 of the
-# survey); each is certified >= DELTA from the spectrum by equal counts at mu -/+ DELTA
-SHIFTS = {"cfg2": [-10.0, 0.37], "cfg3": [0.5, 0.41], "cfg4": [0.5], "cfg5": [0.5, 0.47]}
-GUARD = 100.0  # DELTA = GUARD * eps * max(|lo|, |hi|) of the interval
+# candidate shifts: a grid over the Gershgorin interval; a candidate is kept when its
+# count is non-trivial (0 < neg < n) and equal at mu -/+ DELTA, i.e. it sits in a spectral
+# gap wider than the parity guard (the interior of these spectra is too dense for that,
+# the gaps are near the ends); at most KEEP per config
+NGRID = 48
+KEEP = 2
+GUARD = 10.0  # DELTA = GUARD * eps * max(|lo|, |hi|): the guard of the reference fixtures
 PROD = {"cfg2": (7, 1, 1, 0), "cfg3": (8, 2, 2, 0), "cfg4": (2, 1, 2, 1), "cfg5": (8, 2, 2, 0)}
 
 
@@ -50,19 +53,24 @@ def main():
         torch.cuda.synchronize()
         t_con = time.perf_counter() - t0
         iv = gpu_build.gershgorin_device(H._kernel)
-        cands = [m if m < 0 else iv[0] + m * (iv[1] - iv[0]) for m in SHIFTS[name]]
+        frac = np.concatenate([np.linspace(0.0, 1.0, NGRID + 2)[1:-1]])
+        cands = [float(iv[0] + f * (iv[1] - iv[0])) for f in frac]
         eng = _native.engine_for(H, 0)
         # certify each candidate: equal negative counts at mu - delta, mu, mu + delta means no
         # eigenvalue of the factored matrix within delta (the parity criterion's guard band)
         delta = GUARD * H.eps * max(abs(iv[0]), abs(iv[1]))
-        eng.set_option("max_batch", 8)
+        eng.set_option("max_batch", 7)
         probe = [x for m in cands for x in (m - delta, m, m + delta)]
         pc, _, _ = ldl_counts_array(H, probe)
         mus, rejected = [], []
         for q, m in enumerate(cands):
             negs = [int(pc[3 * q + d, 0]) for d in range(3)]
-            (mus if len(set(negs)) == 1 else rejected).append(m)
-            print(name, "candidate", m, "negatives at -d/0/+d", negs, flush=True)
+            ok = len(set(negs)) == 1 and 0 < negs[0] < cloud.n
+            (mus if ok else rejected).append(m)
+            print(name, "candidate", m, "negatives at -d/0/+d", negs, "ok" if ok else "", flush=True)
+        # prefer one from each end of the spectrum
+        if len(mus) > KEEP:
+            mus = [mus[0], mus[-1]]
         gpu = {}
         for label, (mb, conc, sched, order, budget) in (
                 ("reference_order", (4, 1, 0, 1 if name == "cfg4" else 0, 0)),
