@@ -134,6 +134,74 @@ def measure_fp64_peak(torch, dev):
     return 2.0 * n ** 3 / best / 1e12
 
 
+def measure_int8_peak(torch, dev):
+    """cuBLASLt INT8 GEMM (torch._int_mm, int32 accumulate) 8192^3, best of 5 -> TOPS.
+    None when this torch build has no CUDA int8 GEMM."""
+    n = 8192
+    try:
+        a = torch.randint(-127, 127, (n, n), dtype=torch.int8, device=dev)
+        b = torch.randint(-127, 127, (n, n), dtype=torch.int8, device=dev)
+        torch._int_mm(a, b)
+        torch.cuda.synchronize()
+        best = 1e9
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1) / 1e3)
+        del a, b
+        torch.cuda.empty_cache()
+        return 2.0 * n ** 3 / best / 1e12
+    except Exception:  # noqa: BLE001
+        return None
+
+
+# Ozaki INT8 Schur update: every fp64 multiply-add becomes 36 int8 slice-pair
+# multiply-adds (8 slices per operand, pairs i + j <= 7; k_schur_oz.cu)
+OZ_PAIRS = 36
+DEFAULT_SCHUR_ARITH = 1
+
+
+def schur_roofline(arith, schur_flops, ms_schur, ms, n_local, torch, traffic):
+    """Roofline of the dominant kernel (the K6 Schur update) for the arithmetic in use."""
+    dgemm = measure_fp64_peak(torch, "cuda")
+    t = ms_schur / 1e3
+    fp64_eq = schur_flops / t / 1e12 if t > 0 else None
+    common = {"schur_share_of_step": ms_schur / ms if ms else None,
+              "algorithmic_flops_per_eval": schur_flops / max(1, n_local),
+              "flops_rule": "SURVEY.md §8d: Schur n_R R^2 per elimination step "
+                            "(R = live rows of the panel)",
+              "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
+              "traffic_detail": traffic}
+    if arith != 1:
+        return dict(common, bound="tensor", kernel="schur_sym_kernel (K6 Schur update, DMMA fp64)",
+                    achieved=fp64_eq, peak=dgemm, unit="TFLOP/s",
+                    frac=(fp64_eq / dgemm) if fp64_eq else None,
+                    peak_source="measured in-run: cuBLAS DGEMM fp64 8192^3 best of 5 "
+                                "(MEASURED_PEAKS.json has no fp64 figure)")
+    i8 = measure_int8_peak(torch, "cuda")
+    src = "measured in-run: cuBLASLt INT8 GEMM (torch._int_mm) 8192^3 best of 5"
+    if i8 is None:
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                i8 = 2.0 * float(json.load(f)["bf16_tflops"])
+            src = "2 x MEASURED_PEAKS.json bf16_tflops (burst): the dense INT8 rate is twice bf16"
+        except (OSError, KeyError, ValueError):
+            i8 = 2.0 * 1590.0
+            src = "2 x the profiling recipe's fallback bf16 figure"
+    ach = OZ_PAIRS * schur_flops / t / 1e12 if t > 0 else None
+    return dict(common, bound="tensor",
+                kernel="schur_oz_kernel (K6 Schur update, fp64-accurate Ozaki slices on the INT8 "
+                       "tensor cores, tcgen05.mma.kind::i8; includes oz_split_kernel)",
+                achieved=ach, peak=i8, unit="TFLOP/s", frac=(ach / i8) if ach else None,
+                achieved_rule="int8 ops = 36 slice pairs x the fp64 algorithmic Schur flops",
+                peak_source=src,
+                fp64_equivalent={"achieved_tflops": fp64_eq, "dgemm_peak_tflops": dgemm,
+                                 "ratio_to_dgemm_peak": (fp64_eq / dgemm) if fp64_eq else None})
+
+
 # ------------------------------------------------------------------ workloads
 class Workload:
     name = ""
@@ -241,6 +309,26 @@ def oracle_sample(host_H, mu, seconds, cache):
         return eng.elim_flops, time.perf_counter() - t0, eng._nclus, False
 
 
+FULL_EVAL_FILE = os.path.join(ROOT, "profiles", "r2_cpu_full_evaluations.json")
+
+
+def measured_full_evaluation(name):
+    """A complete CPU factorization of this config, measured on the GPU box's host cores
+    (tools/fullsize_parity.py -> profiles/r2_cpu_full_evaluations.json), or None."""
+    try:
+        with open(FULL_EVAL_FILE) as f:
+            ev = [e for e in json.load(f)["evaluations"] if e["config"] == name]
+    except (OSError, KeyError, ValueError):
+        return None
+    if not ev:
+        return None
+    e = max(ev, key=lambda x: x["elim_flops"])
+    return {"seconds": e["seconds"], "evals_per_s": e["evals_per_s"], "host_threads": e["host_threads"],
+            "elim_flops": e["elim_flops"], "mu": e["mu"],
+            "source": os.path.relpath(FULL_EVAL_FILE, ROOT) + " (oracle port run to completion on the "
+                      "device-built H, same box type)"}
+
+
 def cpu_baseline(wl, mus, elim_per_eval, seconds):
     """Oracle port on the host, bounded sample, scaled to evaluations/s."""
     from paper_2311_08618_b200 import gpu_build
@@ -275,7 +363,7 @@ def cpu_baseline(wl, mus, elim_per_eval, seconds):
                       f"{elim_per_eval / 1e12:.1f} elimination TFLOP; oracle/engine_ref.py on "
                       f"the same H exported to host memory), scaled by the flop fraction",
             "elim_gflops_per_s": rate / 1e9, "extrapolated": True,
-            "setup_s": setup}
+            "setup_s": setup, "full_evaluation_measured": measured_full_evaluation(wl.name)}
 
 
 # ----------------------------------------------------------------------- ours
@@ -309,8 +397,10 @@ def run_ours(args):
     wl.config["waves"] = f"{conc} concurrent wave(s) of <= {(S + conc - 1) // conc} shifts"
     sched = args.schedule if args.schedule >= 0 else (1 if wl.name in ("cfg1", "cfg2") else 2)
     eng.set_option("schedule", sched)
-    if args.schur_arith >= 0:
-        eng.set_option("schur_arith", args.schur_arith)
+    arith = args.schur_arith if args.schur_arith >= 0 else DEFAULT_SCHUR_ARITH
+    eng.set_option("schur_arith", arith)
+    wl.config["schur_arithmetic"] = {0: "fp64 DMMA (mma.sync)",
+                                     1: "fp64-accurate Ozaki slices on INT8 tcgen05"}[arith]
     wl.config["schedule"] = {0: "one cluster at a time, ascending (the reference)",
                              1: "ascending-order wavefronts (level-batched, reference order)",
                              2: "colour classes (level-batched, re-ordered)"}[sched]
@@ -491,8 +581,6 @@ def run_ours(args):
     if rank != 0:
         dist.destroy_process_group()
         return
-    peak = measure_fp64_peak(torch, "cuda")
-    achieved = schur_flops / (ms_schur / 1e3) / 1e12 if ms_schur > 0 else None
     traffic = None
     try:  # DRAM bytes per Schur launch from the committed ncu --set full capture (config 2)
         with open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")) as f:
@@ -511,17 +599,7 @@ def run_ours(args):
                        parallelism=f"shift-sharded multisection x{world} (NCCL all-gather of counts)"
                        if world > 1 else "single GPU",
                        l2="inputs larger than L2 (H and the per-shift working blocks are GBs)"),
-        "roofline": {"bound": "tensor", "kernel": "schur_sym_kernel (K6 Schur update, DMMA fp64)",
-                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": (achieved / peak) if achieved else None,
-                     "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
-                     "traffic_detail": traffic,
-                     "peak_source": "measured in-run: cuBLAS DGEMM fp64 8192^3 best of 5 "
-                                    "(MEASURED_PEAKS.json has no fp64 figure)",
-                     "schur_share_of_step": ms_schur / ms if ms else None,
-                     "algorithmic_flops_per_eval": schur_flops / max(1, n_local),
-                     "flops_rule": "SURVEY.md §8d: Schur n_R R^2 per elimination step "
-                                   "(R = live rows of the panel)"},
+        "roofline": schur_roofline(arith, schur_flops, ms_schur, ms, n_local, torch, traffic),
         "step_rates": {"algorithmic_tflops": flops / t_dev / 1e12 if t_dev else None,
                        "elimination_tflops": elim / t_dev / 1e12 if t_dev else None,
                        "dmma_executed_tflops": gemm_exec / (ms / 1e3) / 1e12 if ms else None,
@@ -653,7 +731,8 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": cfg,
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": sample},
+                         "sample": sample,
+                         "full_evaluation_measured": measured_full_evaluation(args.config)},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

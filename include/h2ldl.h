@@ -189,7 +189,7 @@ int h2l_comm_destroy(h2l_comm *comm);
  *                 complement gets a different orthonormal basis), 0 full ordering;
  *  "block_cache"  1/0 host free list of same-size blocks;
  *  "schur_arith"  arithmetic of the Schur update (the dominant kernel): 0 fp64 on the
- *                 DMMA pipe (mma.sync), 1 fp64-accurate on the INT8 tensor cores
+ *                 DMMA pipe (mma.sync), 1 (default) fp64-accurate on the INT8 tensor cores
  *                 (tcgen05.mma.kind::i8): each row of X / Bg split into 8 exact
  *                 7-bit slices under a power-of-two row scale, the 36 slice-pair
  *                 products of weight >= 2^-63 summed exactly in int32 tensor memory,

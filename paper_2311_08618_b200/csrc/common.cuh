@@ -11,6 +11,7 @@
 #include <mutex>
 #include <set>
 #include <utility>
+#include <vector>
 #include <cuda_runtime.h>
 
 namespace h2l {
@@ -178,16 +179,17 @@ struct OzJob {
     const double *X, *Bg;
     int64_t sx;
     int ld, R, K, nseg;
-    const int *seg_of, *seg_start;   // seg_of == nullptr: one segment, dense target (tests)
+    const int *seg_of, *seg_start;
     const SchurTarget *tbl;
     int row0;          // first packed row
     int tile0;         // first grid tile
 };
 int schur_oz_tiles(int R);
+void schur_oz_tile_order(int R, int job, std::vector<int2> &out);
 size_t schur_oz_scratch_bytes(int rows_total, int kpad, int nshift);
-cudaError_t launch_schur_oz(const OzJob *jobs, const int *row_job, const int *tile_job,
+cudaError_t launch_schur_oz(const OzJob *jobs, const int *row_job, const int2 *tile_ij,
                             int rows_total, int kpad, int total_tiles, int nshift, void *scratch,
-                            cudaStream_t st, double *dense_out = nullptr, int ld_out = 0, int probe = 0);
+                            cudaStream_t st, int probe = 0);
 void launch_schur_sym(const double *X, const double *Bg, int64_t sx, int ld, int R, int K,
                       const int *seg_of, const int *seg_start, int nseg, const SchurTarget *tbl,
                       int nshift, cudaStream_t st, int variant = 0);

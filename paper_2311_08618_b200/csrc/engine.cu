@@ -283,6 +283,7 @@ public:
             for (double *p : kv.second) cudaFreeAsync(p, st_);
         bcache_.clear();
         bcache_bytes_ = 0;
+        release_oz_scratch();
         for (void *p : {(void *)d_mu_, (void *)d_tol_, (void *)d_dropped_, (void *)d_counts_,
                         (void *)d_status_, (void *)d_rank_})
             if (p) cudaFreeAsync(p, st_);
@@ -325,7 +326,14 @@ private:
     int group_max_ = 512;
     int t_level_max_ = -1;  // largest recompression rank of the current level (-1: none yet)
     bool qr_budget_ = true;
-    int schur_arith_ = 0;             // 0 DMMA fp64, 1 INT8 tensor cores, Ozaki slices (k_schur_oz.cu)
+    int schur_arith_ = 1;             // 0 DMMA fp64, 1 (default) INT8 tensor cores, Ozaki slices (k_schur_oz.cu)
+    void *oz_scratch_ = nullptr;      // slice buffers of the INT8 Schur update (per wave)
+    size_t oz_scratch_cap_ = 0;
+    void release_oz_scratch() {
+        if (oz_scratch_) cudaFreeAsync(oz_scratch_, st_);
+        oz_scratch_ = nullptr;
+        oz_scratch_cap_ = 0;
+    }
     bool uploaded_ = false;
     cudaEvent_t ev_call_[2];
     std::vector<cudaEvent_t> ev_pool_;
@@ -836,6 +844,7 @@ private:
             std::memcpy(counts, hc.data(), sizeof(int64_t) * 3 * s);
             for (int z = 0; z < s; ++z) status[z] = hs[z] ? H2L_SHIFT_SINGULAR : H2L_SHIFT_OK;
         }
+        release_oz_scratch();
         for (double *p : {d_mu_, d_tol_, d_dropped_}) CK(cudaFreeAsync(p, st_));
         CK(cudaFreeAsync(d_counts_, st_));
         CK(cudaFreeAsync(d_status_, st_));
@@ -1762,6 +1771,7 @@ private:
             int oz_rows = 0, oz_kpad = 0;
             std::vector<SchurJob> sj;
             std::vector<int> seg_all, start_all, tile_job;
+            std::vector<int2> tile_ij;
             std::vector<SchurTarget> tbl_all;
             std::vector<size_t> seg_off, start_off, tbl_off;
             int tiles_tot = 0;
@@ -1833,7 +1843,8 @@ private:
                     oz_rows += 128 * rp;
                     oz_kpad = std::max(oz_kpad, (nR + 63) / 64 * 64);
                 }
-                tile_job.insert(tile_job.end(), tl, (int)sj.size() - 1);
+                if (oz) schur_oz_tile_order(j.R, (int)sj.size() - 1, tile_ij);
+                else tile_job.insert(tile_job.end(), tl, (int)sj.size() - 1);
                 tiles_tot += tl;
                 // algorithmic panel work (survey §8d): TRSM R nR^2 + D-scale R nR
                 flops_tot += (double)j.R * nR * nR + (double)j.R * nR + sch;
@@ -1850,7 +1861,8 @@ private:
             const size_t os = pk2.add(seg_all.data(), sizeof(int) * seg_all.size());
             const size_t ost = pk2.add(start_all.data(), sizeof(int) * start_all.size());
             const size_t otb = pk2.add(tbl_all.data(), sizeof(SchurTarget) * tbl_all.size());
-            const size_t otj = pk2.add(tile_job.data(), sizeof(int) * tile_job.size());
+            const size_t otj = oz ? pk2.add(tile_ij.data(), sizeof(int2) * tile_ij.size())
+                                  : pk2.add(tile_job.data(), sizeof(int) * tile_job.size());
             const size_t osj = pk2.add(sj.data(), sizeof(SchurJob) * sj.size());
             const size_t ooz = oz ? pk2.add(ozj.data(), sizeof(OzJob) * ozj.size()) : 0;
             const size_t orj = oz ? pk2.add(row_job.data(), sizeof(int) * row_job.size()) : 0;
@@ -1871,20 +1883,51 @@ private:
             stage_commit(rg);
             char *d2 = rg.d;
             void *scratch = nullptr;
-            if (oz)
-                CK(cudaMallocFromPoolAsync(&scratch, schur_oz_scratch_bytes(oz_rows, oz_kpad, s_), pool_,
-                                           st_));
+            if (oz) {
+                // one slice buffer per wave, grown geometrically (pool growth maps new
+                // physical memory: not something to do per launch)
+                const size_t need = schur_oz_scratch_bytes(oz_rows, oz_kpad, s_);
+                if (need > oz_scratch_cap_) {
+                    if (oz_scratch_) CK(cudaFreeAsync(oz_scratch_, st_));
+                    oz_scratch_cap_ = std::max(need, oz_scratch_cap_ + oz_scratch_cap_ / 2);
+                    CK(cudaMallocFromPoolAsync(&oz_scratch_, oz_scratch_cap_, pool_, st_));
+                }
+                scratch = oz_scratch_;
+            }
+            static const bool schurlog = getenv("H2L_SCHURLOG") != nullptr;
+            cudaEvent_t lg0 = nullptr, lg1 = nullptr;
+            if (schurlog) {
+                CK(cudaEventCreate(&lg0));
+                CK(cudaEventCreate(&lg1));
+                CK(cudaEventRecord(lg0, st_));
+            }
             {
                 Timed tm(this, 1);
                 if (oz)
                     CK(launch_schur_oz((const OzJob *)(d2 + ooz), (const int *)(d2 + orj),
-                                       (const int *)(d2 + otj), oz_rows, oz_kpad, tiles_tot, s_, scratch,
+                                       (const int2 *)(d2 + otj), oz_rows, oz_kpad, tiles_tot, s_, scratch,
                                        st_));
                 else
                     launch_schur_sym_multi((const SchurJob *)(d2 + osj), (const int *)(d2 + otj),
                                            tiles_tot, s_, st_);
             }
-            if (scratch) CK(cudaFreeAsync(scratch, st_));
+            if (schurlog) {
+                CK(cudaEventRecord(lg1, st_));
+                CK(cudaEventSynchronize(lg1));
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, lg0, lg1));
+                int rmax = 0, kmax = 0;
+                double fl = 0.0;
+                for (auto &q : sj) {
+                    rmax = std::max(rmax, q.R);
+                    kmax = std::max(kmax, q.K);
+                    fl += (double)q.R * q.R * q.K;
+                }
+                fprintf(stderr, "schurlog arith=%d jobs=%zu Rmax=%d Kmax=%d tiles=%d shifts=%d ms=%.3f tflops=%.1f\n",
+                        (int)oz, sj.size(), rmax, kmax, tiles_tot, s_, ms, fl * s_ / (ms * 1e-3) / 1e12);
+                cudaEventDestroy(lg0);
+                cudaEventDestroy(lg1);
+            }
             CK(cudaGetLastError());
             dbg_sync("schur-sym");
             st_acc_->launches++;

@@ -30,7 +30,9 @@
 #include <cuda.h>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "tcgen05.cuh"
@@ -65,21 +67,6 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
 // instruction descriptor: kind::i8, s32 accumulate, signed A/B, both K-major, M=128, N=n
 __host__ __device__ constexpr uint32_t idesc_n(int n) {
     return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-}
-
-// tile t of a job with R rows -> (I, J): row tile I (128), column tile J (64), J >= 2I
-__device__ __forceinline__ void tri_tile_oz(int t, int R, int &I, int &J) {
-    const int NJ = (R + BN - 1) / BN;
-    I = 0;
-    while (true) {
-        const int cnt = NJ - 2 * I;
-        if (t < cnt) {
-            J = 2 * I + t;
-            return;
-        }
-        t -= cnt;
-        ++I;
-    }
 }
 
 }  // namespace oz
@@ -157,9 +144,8 @@ __device__ __forceinline__ double pow2i(int e) {
 __global__ void __launch_bounds__(oz::THREADS, 1)
     schur_oz_kernel(const __grid_constant__ CUtensorMap map_x,
                     const __grid_constant__ CUtensorMap map_b, const OzJob *jobs,
-                    const int *tile_job, int total_tiles, int nshift, int rows_total,
-                    const int *ex_all, const int *eb_all, double *dense_out, int ld_out,
-                    int probe) {
+                    const int2 *tile_ij, int total_tiles, int nshift, int rows_total,
+                    const int *ex_all, const int *eb_all, int probe) {
     using namespace oz;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -201,12 +187,10 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
 
     auto locate = [&](int item, OzJob &jb, int &z, int &m0, int &n0) {
         z = item / total_tiles;
-        const int t = item - z * total_tiles;
-        jb = jobs[tile_job[t]];
-        int I, J;
-        tri_tile_oz(t - jb.tile0, jb.R, I, J);
-        m0 = I * BM;
-        n0 = J * BN;
+        const int2 tj = tile_ij[item - z * total_tiles];
+        jb = jobs[tj.x];
+        m0 = (tj.y >> 16) * BM;
+        n0 = (tj.y & 0xFFFF) * BN;
     };
 
     if (warp == 0) {
@@ -285,8 +269,8 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
             asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
             for (int x = t; x < BM + BN; x += 32 * EPI_WARPS) {
                 const int g = x < BM ? m0 + x : n0 + (x - BM);
-                const int sg = g < jb.R ? (jb.seg_of ? jb.seg_of[g] : 0) : -1;
-                const int off = sg >= 0 ? (jb.seg_of ? g - jb.seg_start[sg] : g) : 0;
+                const int sg = g < jb.R ? jb.seg_of[g] : -1;
+                const int off = sg >= 0 ? g - jb.seg_start[sg] : 0;
                 if (x < BM) {
                     s_rseg[x] = sg;
                     s_roff[x] = off;
@@ -297,6 +281,21 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
                     s_sc[x - BM] = pow2i(eb_all[(size_t)z * rows_total + jb.row0 + g]);
                 }
             }
+            asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
+            if (t == 0) {
+                const int rlast = min(BM, jb.R - m0) - 1, clast = min(BN, jb.R - n0) - 1;
+                s_box[0] = s_rseg[0];
+                s_box[1] = s_rseg[rlast] - s_rseg[0] + 1;
+                s_box[2] = s_cseg[0];
+                s_box[3] = s_cseg[clast] - s_cseg[0] + 1;
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
+            const int alo = s_box[0], na = s_box[1], blo = s_box[2], nb = s_box[3];
+            const bool in_smem = na * nb <= MAXT;
+            if (in_smem)
+                for (int e = t; e < na * nb; e += 32 * EPI_WARPS)
+                    s_tbl[e] = jb.tbl[(size_t)(alo + e / nb) * jb.nseg + blo + e % nb];
+            asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
             mbar_wait(tfull, it & 1);
             tc_fence_after();
             double acc[32];
@@ -317,47 +316,55 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
             const double sr = s_sr[rl];
 #pragma unroll
             for (int c = 0; c < 32; ++c) ct[rl * CT_LD + h * 32 + c] = acc[c] * sr;
-            if (t == 0 && !dense_out) {
-                const int rlast = min(BM, jb.R - m0) - 1, clast = min(BN, jb.R - n0) - 1;
-                s_box[0] = s_rseg[0];
-                s_box[1] = s_rseg[rlast] - s_rseg[0] + 1;
-                s_box[2] = s_cseg[0];
-                s_box[3] = s_cseg[clast] - s_cseg[0] + 1;
-            }
             asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
-            if (dense_out) {
-                // test path: dense C (R x ld_out per shift) = X Bg^T on the upper triangle
-                for (int e = t; e < BM * BN; e += 32 * EPI_WARPS) {
-                    const int r = e / BN, c = e % BN;
-                    if (m0 + r < jb.R && n0 + c < jb.R && n0 + c >= m0 + r)
-                        dense_out[(size_t)z * jb.R * ld_out + (size_t)(m0 + r) * ld_out + n0 + c] =
-                            ct[r * CT_LD + c] * s_sc[c];
-                }
-                continue;
+            // warp w: rows w, w + 8, ...; lane: columns lane, lane + 32 (row-contiguous
+            // REDs).  A lane's two columns are fixed for the tile: their segment, offset
+            // and scale are hoisted, and the target of (row segment, column segment) is
+            // re-read only when the row segment changes (a tile spans a few segments).
+            int cb2[2], bseg[2];
+            double sc2[2];
+            bool live[2];
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const int cl = hh * 32 + lane;
+                bseg[hh] = s_cseg[cl];
+                cb2[hh] = s_coff[cl];
+                sc2[hh] = -s_sc[cl];
+                live[hh] = bseg[hh] >= 0;
             }
-            const int alo = s_box[0], na = s_box[1], blo = s_box[2], nb = s_box[3];
-            const bool in_smem = na * nb <= MAXT;
-            if (in_smem)
-                for (int e = t; e < na * nb; e += 32 * EPI_WARPS)
-                    s_tbl[e] = jb.tbl[(size_t)(alo + e / nb) * jb.nseg + blo + e % nb];
-            asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
-            // warp w: rows w, w + 8, ...; lane: columns lane, lane + 32 (row-contiguous REDs)
+            int a_cur = -1;
+            double *tb[2] = {nullptr, nullptr};
+            int64_t tld[2] = {0, 0};
+            bool ttr[2] = {false, false}, mir[2] = {false, false};
             for (int r = ew; r < BM; r += EPI_WARPS) {
                 const int gr = m0 + r, a = s_rseg[r], ra = s_roff[r];
                 if (a < 0) break;
+                if (a != a_cur) {
+                    a_cur = a;
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        tb[hh] = nullptr;
+                        if (!live[hh]) continue;
+                        const int b = bseg[hh];
+                        const SchurTarget e = in_smem ? s_tbl[(a - alo) * nb + (b - blo)]
+                                                      : jb.tbl[(size_t)a * jb.nseg + b];
+                        if (!e.base) continue;
+                        tb[hh] = e.base + z * e.bs;
+                        tld[hh] = e.ldc;
+                        ttr[hh] = e.trans != 0;
+                        mir[hh] = a == b;
+                    }
+                }
+                if (probe == 4) continue;  // benchmarking only: no reductions
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
-                    const int cl = hh * 32 + lane, gc = n0 + cl;
-                    const int b = s_cseg[cl], cb = s_coff[cl];
-                    if (b < 0 || gc < gr) continue;
-                    const SchurTarget e = in_smem ? s_tbl[(a - alo) * nb + (b - blo)]
-                                                  : jb.tbl[(size_t)a * jb.nseg + b];
-                    if (!e.base) continue;
-                    const double val = ct[r * CT_LD + cl] * s_sc[cl];
-                    double *base = e.base + z * e.bs;
-                    red_add_f64(base + (e.trans ? (int64_t)cb * e.ldc + ra : (int64_t)ra * e.ldc + cb),
-                                -val);
-                    if (a == b && cb != ra) red_add_f64(base + (int64_t)cb * e.ldc + ra, -val);
+                    const int cl = hh * 32 + lane;
+                    if (!tb[hh] || n0 + cl < gr) continue;
+                    const double val = ct[r * CT_LD + cl] * sc2[hh];
+                    const int cb = cb2[hh];
+                    red_add_f64(tb[hh] + (ttr[hh] ? (int64_t)cb * tld[hh] + ra : (int64_t)ra * tld[hh] + cb),
+                                val);
+                    if (mir[hh] && cb != ra && probe != 3) red_add_f64(tb[hh] + (int64_t)cb * tld[hh] + ra, val);
                 }
             }
         }
@@ -410,11 +417,27 @@ size_t schur_oz_scratch_bytes(int rows_total, int kpad, int nshift) {
     return 2 * sl + 2 * ((ex + 255) / 256 * 256);
 }
 
-// jobs / row_job / tile_job are device arrays (row_job: one entry per 128 packed rows);
+// Grid tiles of one job in the launch order: column blocks of OZ_JB column tiles
+// (64 rows of Bg each); within a block, row tiles ascending, then the block's column
+// tiles.  Concurrent CTAs then share one block of Bg slices (L2-resident) and stream
+// the X slices once per block, instead of re-reading every Bg tile once per row tile
+// (the panels reach 60k rows: their slices are GBs, far above L2).
+constexpr int OZ_JB = 64;
+void schur_oz_tile_order(int R, int job, std::vector<int2> &out) {
+    const int NJ = (R + oz::BN - 1) / oz::BN;
+    for (int j0 = 0; j0 < NJ; j0 += OZ_JB) {
+        const int j1 = std::min(NJ, j0 + OZ_JB);
+        for (int I = 0; 2 * I < j1; ++I)
+            for (int J = std::max(j0, 2 * I); J < j1; ++J) out.push_back(make_int2(job, (I << 16) | J));
+    }
+}
+
+// jobs / row_job / tile_ij are device arrays (row_job: one entry per 128 packed rows,
+// tile_ij: (job, I << 16 | J) per grid tile in launch order, schur_oz_tile_order);
 // scratch holds schur_oz_scratch_bytes(rows_total, kpad, nshift) bytes.
-cudaError_t launch_schur_oz(const OzJob *jobs, const int *row_job, const int *tile_job,
+cudaError_t launch_schur_oz(const OzJob *jobs, const int *row_job, const int2 *tile_ij,
                             int rows_total, int kpad, int total_tiles, int nshift, void *scratch,
-                            cudaStream_t st, double *dense_out, int ld_out, int probe) {
+                            cudaStream_t st, int probe) {
     if (total_tiles <= 0 || nshift <= 0 || rows_total <= 0) return cudaSuccess;
     if (kpad % 64 || rows_total % oz::BM) return cudaErrorInvalidValue;
     const size_t sl = (size_t)oz::SLICES * rows_total * kpad * nshift;
@@ -440,7 +463,7 @@ cudaError_t launch_schur_oz(const OzJob *jobs, const int *row_job, const int *ti
     }
     const int items = total_tiles * nshift;
     schur_oz_kernel<<<items < nsm ? items : nsm, oz::THREADS, oz::SMEM, st>>>(
-        mx, mb, jobs, tile_job, total_tiles, nshift, rows_total, exr, ebr, dense_out, ld_out, probe);
+        mx, mb, jobs, tile_ij, total_tiles, nshift, rows_total, exr, ebr, probe);
     return cudaGetLastError();
 }
 

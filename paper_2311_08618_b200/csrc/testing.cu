@@ -288,10 +288,11 @@ extern "C" int h2l_internal_gemm_check(int device, int M, int N, int K, int ntas
     });
 }
 
-// INT8-tensor-core (Ozaki) Schur product on dense inputs: for each of `nshift`
-// shifts, X and Bg (R x K row-major, host, shift-major) -> C = X Bg^T on the upper
-// triangle (c >= r; C is R x R, host, lower triangle left untouched).  reps > 0
-// times `reps` launches (split + GEMM) and returns the mean in *ms_out.
+// INT8-tensor-core (Ozaki) Schur update on dense inputs through the production
+// epilogue: one segment whose target is C itself, so for each of `nshift` shifts
+// C -= X Bg^T (X, Bg: R x K row-major, host, shift-major; C: R x R, host) on the upper
+// triangle and, the segment being diagonal, the mirrored lower triangle.  reps > 0
+// times `reps` further launches (split + GEMM, C keeps accumulating) -> mean ms.
 extern "C" int h2l_internal_schur_oz(int device, int R, int K, int nshift, const double *X,
                                      const double *Bg, double *C, int reps, double *ms_out,
                                      int probe) {
@@ -306,20 +307,34 @@ extern "C" int h2l_internal_schur_oz(int device, int R, int K, int nshift, const
         CK(cudaMemcpy(dx, X, sizeof(double) * rk * nshift, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(db, Bg, sizeof(double) * rk * nshift, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(dc, C, sizeof(double) * rr * nshift, cudaMemcpyHostToDevice));
+        std::vector<int> seg(R, 0);
+        int start0 = 0;
+        h2l::SchurTarget tgt{dc, rr, R, 0};
+        int *dseg, *dstart;
+        h2l::SchurTarget *dtbl;
+        CK(cudaMalloc(&dseg, sizeof(int) * std::max(1, R)));
+        CK(cudaMalloc(&dstart, sizeof(int)));
+        CK(cudaMalloc(&dtbl, sizeof(tgt)));
+        CK(cudaMemcpy(dseg, seg.data(), sizeof(int) * R, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dstart, &start0, sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dtbl, &tgt, sizeof(tgt), cudaMemcpyHostToDevice));
         h2l::OzJob jb{};
         jb.X = dx; jb.Bg = db; jb.sx = rk; jb.ld = K; jb.R = R; jb.K = K; jb.nseg = 1;
+        jb.seg_of = dseg; jb.seg_start = dstart; jb.tbl = dtbl;
         jb.row0 = 0; jb.tile0 = 0;
         const int tiles = h2l::schur_oz_tiles(R);
-        std::vector<int> row_job(rpad / 128, 0), tile_job(tiles, 0);
-        h2l::OzJob *djob; int *drj, *dtj; void *scratch;
+        std::vector<int> row_job(rpad / 128, 0);
+        std::vector<int2> tile_ij;
+        h2l::schur_oz_tile_order(R, 0, tile_ij);
+        h2l::OzJob *djob; int *drj; int2 *dtj; void *scratch;
         CK(cudaMalloc(&djob, sizeof(jb)));
         CK(cudaMalloc(&drj, sizeof(int) * row_job.size()));
-        CK(cudaMalloc(&dtj, sizeof(int) * std::max(1, tiles)));
+        CK(cudaMalloc(&dtj, sizeof(int2) * std::max(1, tiles)));
         CK(cudaMalloc(&scratch, h2l::schur_oz_scratch_bytes(rpad, kpad, nshift)));
         CK(cudaMemcpy(djob, &jb, sizeof(jb), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(drj, row_job.data(), sizeof(int) * row_job.size(), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(dtj, tile_job.data(), sizeof(int) * tiles, cudaMemcpyHostToDevice));
-        CK(h2l::launch_schur_oz(djob, drj, dtj, rpad, kpad, tiles, nshift, scratch, 0, dc, R));
+        CK(cudaMemcpy(dtj, tile_ij.data(), sizeof(int2) * tiles, cudaMemcpyHostToDevice));
+        CK(h2l::launch_schur_oz(djob, drj, dtj, rpad, kpad, tiles, nshift, scratch, 0));
         CK(cudaDeviceSynchronize());
         CK(cudaMemcpy(C, dc, sizeof(double) * rr * nshift, cudaMemcpyDeviceToHost));
         if (reps > 0 && ms_out) {
@@ -328,8 +343,7 @@ extern "C" int h2l_internal_schur_oz(int device, int R, int K, int nshift, const
             CK(cudaEventCreate(&e1));
             CK(cudaEventRecord(e0));
             for (int q = 0; q < reps; ++q)
-                CK(h2l::launch_schur_oz(djob, drj, dtj, rpad, kpad, tiles, nshift, scratch, 0, dc, R,
-                                        probe));
+                CK(h2l::launch_schur_oz(djob, drj, dtj, rpad, kpad, tiles, nshift, scratch, 0, probe));
             CK(cudaEventRecord(e1));
             CK(cudaEventSynchronize(e1));
             float ms = 0.f;
@@ -338,8 +352,9 @@ extern "C" int h2l_internal_schur_oz(int device, int R, int K, int nshift, const
             cudaEventDestroy(e0);
             cudaEventDestroy(e1);
         }
-        cudaFree(dx); cudaFree(db); cudaFree(dc); cudaFree(djob); cudaFree(drj); cudaFree(dtj);
-        cudaFree(scratch);
+        for (void *p : {(void *)dx, (void *)db, (void *)dc, (void *)djob, (void *)drj, (void *)dtj,
+                        scratch, (void *)dseg, (void *)dstart, (void *)dtbl})
+            cudaFree(p);
     });
 }
 

@@ -390,3 +390,53 @@ def config_device(name, seed=0, n=None, leaf=None, device="cuda", verbose=False)
     H = construct_device(kern, tree, st, cfg.eps, device=device, verbose=verbose)
     H._kernel = kern
     return H, cloud
+
+
+def reconstruct_dense_device(H, device="cuda"):
+    """Dense realisation of an unshifted device-built H on the GPU (validation only:
+    the reference's `reconstruct_dense`, compress.py / h2matrix.reconstruct_dense, for
+    sizes whose n x n fp64 matrix fits in HBM -- config 2 is 34 GB)."""
+    t = _torch()
+    tree = H.tree
+    L = tree.depth
+    n = H.n
+    dev = t.device(device)
+    A = t.zeros((n, n), dtype=t.float64, device=dev)
+
+    def dv(x):
+        return x if isinstance(x, t.Tensor) else t.as_tensor(np.asarray(x), dtype=t.float64,
+                                                              device=dev)
+
+    for i, blk in H.leaf_diag.items():
+        lo, hi = tree.index_range(L, i)
+        A[lo:hi, lo:hi] = dv(blk)
+    for (i, j), blk in H.leaf_offdiag.items():
+        (a0, a1), (b0, b1) = tree.index_range(L, i), tree.index_range(L, j)
+        b = dv(blk)
+        A[a0:a1, b0:b1] = b
+        A[b0:b1, a0:a1] = b.T
+    memo = {}
+
+    def expanded(level, i):
+        key = (level, i)
+        if key not in memo:
+            bs = H.bases[key]
+            if tree.is_leaf_level(level):
+                memo[key] = dv(bs.U_S)
+            else:
+                (lc, c1), (_, c2) = tree.children(level, i)
+                e1, e2 = expanded(lc, c1), expanded(lc, c2)
+                r1 = e1.shape[1]
+                us = dv(bs.U_S)
+                memo[key] = t.cat([e1 @ us[:r1], e2 @ us[r1:]], dim=0)
+        return memo[key]
+
+    for (level, i, j), S in sorted(H.couplings.items(), key=lambda kv: -kv[0][0]):
+        ei, ej = expanded(level, i), expanded(level, j)
+        (a0, a1), (b0, b1) = tree.index_range(level, i), tree.index_range(level, j)
+        blk = ei @ dv(S) @ ej.T
+        A[a0:a1, b0:b1] = blk
+        A[b0:b1, a0:a1] = blk.T
+        del blk
+    memo.clear()
+    return A

@@ -17,7 +17,7 @@ f = lib.h2l_internal_schur_oz
 f.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _f64p, _f64p, _f64p,
               ctypes.c_int, _f64p, ctypes.c_int]
 probes = [int(a) for a in sys.argv[1:]] or [0]
-for (s, R, K) in [(1, 2048, 256), (1, 4096, 448), (4, 4096, 448), (7, 4096, 448), (1, 8192, 448)]:
+for (s, R, K) in [(7, 4096, 448), (7, 16384, 160), (7, 16384, 256), (2, 40960, 192)]:
     rng = np.random.default_rng(0)
     X = rng.standard_normal((s, R, K))
     B = rng.standard_normal((s, R, K))
