@@ -299,7 +299,7 @@ def payload_digest(H):
 
 
 # ------------------------------------------------------------- payload file IO
-def save_payload(path, H):
+def save_payload(path, H, compress=True):
     """Serialise the origin payload of H (tree ranges, structure, blocks) to .npz."""
     org = H.origin()
     tree, st = org.tree, org.structure
@@ -323,7 +323,7 @@ def save_payload(path, H):
         out[f"r_{l}_{i}"] = np.array(bs.rank)
     for (l, i, j), blk in org.couplings.items():
         out[f"C_{l}_{i}_{j}"] = blk
-    np.savez_compressed(path, **out)
+    (np.savez_compressed if compress else np.savez)(path, **out)
 
 
 def load_payload(path):
