@@ -681,6 +681,8 @@ def run_reference(args):
                 pool.map(_ref_cfg1_worker, [([rng.uniform(lo, hi)],) for _ in range(cores)])
             dt = time.perf_counter() - t0
         v = cores * K / dt
+        step_ms = 1e3 * dt / K
+        units_per_step = cores
         sample = (f"{cores} worker processes x 1 whole factorization per step "
                   f"(oracle/engine_ref.py, OPENBLAS_NUM_THREADS=1)")
         cfg = {"workload": "cfg1", "n": 2048, "leaf": 128, "eps": 1e-8}
@@ -720,18 +722,22 @@ def run_reference(args):
             fl_tot += fl
             t_tot += dt
         v = fl_tot / t_tot / elim_per_eval
+        step_ms = 1e3 * t_tot / max(1, K)
+        units_per_step = fl_tot / max(1, K) / elim_per_eval
         cores = _blas_threads()
         sample = (f"each step = first {per:.0f} s of one cfg2 factorization (oracle/engine_ref.py, "
-                  f"numpy BLAS on {cores} threads, same H exported to host), scaled by the "
-                  f"elimination-flop fraction (total per evaluation from {src})")
+                  f"numpy BLAS on {cores} threads, same H exported to host) = "
+                  f"{units_per_step:.4f} of an evaluation by elimination flops (total per "
+                  f"evaluation from {src}); value = evaluations-equivalent / s (extrapolated: a "
+                  f"complete factorization takes ~12 min, full_evaluation_measured)")
         cfg = dict(wl.config)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": K, "warmup": W, "ms_per_step": 1e3 / v if v else None,
+        "steps": K, "warmup": W, "ms_per_step": step_ms, "evaluations_per_step": units_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": cfg,
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": sample,
+                         "sample": sample, "extrapolated": args.config != "cfg1",
                          "full_evaluation_measured": measured_full_evaluation(args.config)},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

@@ -98,6 +98,14 @@ class DeviceKernel:
             return out
         return f
 
+    def rows_at(self, idx, j0, j1):
+        """K(idx, j0:j1) for a device index vector idx disjoint from [j0, j1) (no diagonal)."""
+        t = self.t
+        if self.X is None:
+            return self.A[idx, j0:j1]
+        d = self.X[idx][:, None, :] - self.X[j0:j1][None, :, :]
+        return _radial(self.kind, t.sqrt((d * d).sum(dim=2)), self.kernel, t)
+
     def block_ranges(self, I, J):
         """K over unions of ranges: I, J lists of (start, stop)."""
         t = self.t
@@ -142,7 +150,38 @@ def _partners(tree, st, level):
     return _admissible_matrix(tree, level, st.eta)
 
 
+def _index_vector(ranges, t, dev):
+    if not ranges:
+        return t.zeros(0, dtype=t.int64, device=dev)
+    return t.cat([t.arange(a, b, device=dev) for (a, b) in ranges])
+
+
 # ------------------------------------------------------------- rank reveal
+class _Prof:
+    """Phase timer of the construction (H2L_BUILD_PROFILE=1: synchronising, diagnostics only)."""
+
+    def __init__(self, t):
+        import os
+        import time
+
+        self.on = bool(os.environ.get("H2L_BUILD_PROFILE"))
+        self.t, self.time = t, time
+        self.acc = {}
+        self.last = None
+
+    def __call__(self, what):
+        if not self.on:
+            return
+        self.t.cuda.synchronize()
+        now = self.time.perf_counter()
+        if self.last is not None:
+            self.acc[self.last[0]] = self.acc.get(self.last[0], 0.0) + now - self.last[1]
+        self.last = (what, now)
+
+
+_PROF = None
+
+
 def _split(M_T, eps, t):
     """Basis split of M (rows x cols) given M^T (cols x rows); reference rank rule."""
     m = M_T.shape[1]
@@ -150,11 +189,15 @@ def _split(M_T, eps, t):
     if M_T.shape[0] == 0 or not bool((M_T != 0).any()):
         return t.zeros((m, 0), dtype=t.float64, device=dev), t.eye(m, dtype=t.float64, device=dev)
     colmax = float(t.linalg.vector_norm(M_T, dim=1).max())
+    if _PROF:
+        _PROF("qr")
     if M_T.shape[0] > m:
         R = t.linalg.qr(M_T, mode="r")[1]          # M^T = Q R  ->  M = R^T Q^T
         core = R.T
     else:
         core = M_T.T
+    if _PROF:
+        _PROF("svd")
     U, S, _ = t.linalg.svd(core, full_matrices=True)
     tail = t.sqrt(t.flip(t.cumsum(t.flip(S * S, [0]), 0), [0]))
     hits = t.nonzero(tail <= eps * colmax)
@@ -179,6 +222,8 @@ def construct_device(kernel, tree, structure, eps, device="cuda", verbose=False)
     dev = K.dev
     L = tree.depth
     rng = tree.ranges
+    global _PROF
+    prof = _PROF = _Prof(t)
 
     # ---- bases
     bases = {}
@@ -192,9 +237,11 @@ def construct_device(kernel, tree, structure, eps, device="cuda", verbose=False)
                                  t.zeros((0, 0), dtype=t.float64, device=dev))
                 expanded[(L, i)] = t.zeros((0, 0), dtype=t.float64, device=dev)
                 continue
+            prof("leaf_sample")
             J = [rng[L][j] for j in np.nonzero(part[i])[0]]
-            slabs = [K.block(j0, j1, i0, i1) for (j0, j1) in J]   # K(J, I) = K(I, J)^T
-            MT = t.cat(slabs, dim=0) if slabs else t.zeros((0, i1 - i0), dtype=t.float64, device=dev)
+            jidx = _index_vector(J, t, dev)                        # K(J, I) = K(I, J)^T
+            MT = K.rows_at(jidx, i0, i1) if jidx.numel() else t.zeros((0, i1 - i0), dtype=t.float64,
+                                                                        device=dev)
             US, UR = _split(MT, eps, t)
             bases[(L, i)] = (US, UR)
             expanded[(L, i)] = US
@@ -202,18 +249,18 @@ def construct_device(kernel, tree, structure, eps, device="cuda", verbose=False)
             for level in range(L - 1, 0, -1):
                 part = _partners(tree, st, level)
                 for i in range(tree.num_clusters(level)):
+                    prof("transfer_sample")
                     c1, c2 = 2 * i, 2 * i + 1
                     e1, e2 = expanded[(level + 1, c1)], expanded[(level + 1, c2)]
                     (a0, a1), (b0, b1) = rng[level + 1][c1], rng[level + 1][c2]
                     r1, r2 = e1.shape[1], e2.shape[1]
                     cols = []
-                    for j in np.nonzero(part[i])[0]:
-                        j0, j1 = rng[level][j]
-                        for s0 in range(j0, j1, SLAB):
-                            s1 = min(j1, s0 + SLAB)
-                            top = e1.T @ K.block(a0, a1, s0, s1)
-                            bot = e2.T @ K.block(b0, b1, s0, s1)
-                            cols.append(t.cat([top, bot], dim=0).T)
+                    # all partners' columns at once, in slabs (K(J, I) with I = the two
+                    # children's contiguous rows, split into e1^T / e2^T projections)
+                    jidx = _index_vector([rng[level][j] for j in np.nonzero(part[i])[0]], t, dev)
+                    for s0 in range(0, jidx.numel(), SLAB):
+                        KT = K.rows_at(jidx[s0:s0 + SLAB], a0, b1)      # slab x (m1 + m2)
+                        cols.append(t.cat([KT[:, :a1 - a0] @ e1, KT[:, b0 - a0:] @ e2], dim=1))
                     ZT = t.cat(cols, dim=0) if cols else t.zeros((0, r1 + r2), dtype=t.float64,
                                                                    device=dev)
                     if r1 + r2 == 0:
@@ -222,8 +269,10 @@ def construct_device(kernel, tree, structure, eps, device="cuda", verbose=False)
                     else:
                         US, UR = _split(ZT, eps, t)
                     bases[(level, i)] = (US, UR)
+                    prof("transfer_expand")
                     expanded[(level, i)] = t.cat([e1 @ US[:r1], e2 @ US[r1:]], dim=0)
 
+    prof("arena")
     # ---- arena layout (the order of _native.build_plan)
     sizes = []
     nleaf = tree.num_clusters(L)
@@ -253,6 +302,7 @@ def construct_device(kernel, tree, structure, eps, device="cuda", verbose=False)
         return arena[o:o + shape[0] * shape[1]].view(shape)
 
     leaf_diag, leaf_offdiag, couplings, bsplit = {}, {}, {}, {}
+    prof("dense_blocks")
     for i in range(nleaf):
         i0, i1 = rng[L][i]
         v = view("D", i, (i1 - i0, i1 - i0))
@@ -264,6 +314,7 @@ def construct_device(kernel, tree, structure, eps, device="cuda", verbose=False)
         v = view("O", (i, j), (i1 - i0, j1 - j0))
         K.block(i0, i1, j0, j1, out=v)
         leaf_offdiag[(i, j)] = v
+    prof("couplings")
     for key in low:
         l, i, j = key
         ei, ej = expanded[(l, i)], expanded[(l, j)]
@@ -275,6 +326,7 @@ def construct_device(kernel, tree, structure, eps, device="cuda", verbose=False)
             acc += K.block(i0, i1, s0, s1) @ ej[s0 - j0:s1 - j0]
         v.copy_(ei.T @ acc)
         couplings[key] = v
+    prof("bases_out")
     for key in sorted(bases):
         US, UR = bases[key]
         m = US.shape[0] if US.numel() else UR.shape[0]
@@ -288,6 +340,9 @@ def construct_device(kernel, tree, structure, eps, device="cuda", verbose=False)
                              leaf_offdiag=leaf_offdiag, bases=bsplit, couplings=couplings)
     H._arena = arena
     H._arena_offsets = offsets
+    prof("end")
+    H._build_profile = dict(prof.acc)
+    _PROF = None
     scale = max((float(b.abs().max()) for b in leaf_diag.values() if b.numel()), default=0.0)
     H._scale0 = scale
     # hand the construction's temporaries back to the device: the engine allocates

@@ -64,7 +64,6 @@ def _instance(name):
         assert out.returncode == 0, out.stderr[-2000:]
         H = load_payload(path)
         shutil.rmtree(tmp, ignore_errors=True)
-        _cache.clear()
         _cache[name] = (H, z, cfg, out.stdout.strip().splitlines()[-1])
     return _cache[name]
 

@@ -20,12 +20,10 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-# candidate shifts: a grid over the Gershgorin interval; a candidate is kept when its
-# count is non-trivial (0 < neg < n) and equal at mu -/+ DELTA, i.e. it sits in a spectral
-# gap wider than the parity guard (the interior of these spectra is too dense for that,
-# the gaps are near the ends); at most KEEP per config
-NGRID = 48
-KEEP = 2
+# shifts: one across the widest gap among the ENDS lowest eigenvalues and one across the
+# widest among the ENDS highest (the interior of these spectra is too dense for gaps wider
+# than the parity guard DELTA); counts there are non-trivial (k and n - k negatives)
+ENDS = 4
 GUARD = 10.0  # DELTA = GUARD * eps * max(|lo|, |hi|): the guard of the reference fixtures
 PROD = {"cfg2": (7, 1, 1, 0), "cfg3": (8, 2, 2, 0), "cfg4": (2, 1, 2, 1), "cfg5": (8, 2, 2, 0)}
 
@@ -34,7 +32,8 @@ def main():
     import torch
 
     from oracle import engine_ref
-    from paper_2311_08618_b200 import _native, gpu_build
+    from paper_2311_08618_b200 import _native, gpu_build, multisection
+    from paper_2311_08618_b200.bisection import InertiaCache
     from paper_2311_08618_b200.ldl import ldl_counts_array
 
     out_path = "gpurun_out/fullsize.json"
@@ -53,28 +52,43 @@ def main():
         torch.cuda.synchronize()
         t_con = time.perf_counter() - t0
         iv = gpu_build.gershgorin_device(H._kernel)
-        frac = np.concatenate([np.linspace(0.0, 1.0, NGRID + 2)[1:-1]])
-        cands = [float(iv[0] + f * (iv[1] - iv[0])) for f in frac]
         eng = _native.engine_for(H, 0)
-        # certify each candidate: equal negative counts at mu - delta, mu, mu + delta means no
-        # eigenvalue of the factored matrix within delta (the parity criterion's guard band)
         delta = GUARD * H.eps * max(abs(iv[0]), abs(iv[1]))
-        eng.set_option("max_batch", 7)
-        probe = [x for m in cands for x in (m - delta, m, m + delta)]
-        pc, _, _ = ldl_counts_array(H, probe)
+        eng.set_option("max_batch", 8)
+        eng.set_option("concurrency", 1)
+        # locate the J lowest and J highest eigenvalues of the factored matrix to a quarter of
+        # the guard (device multisection); a shift midway across a gap wider than 3 delta has
+        # no eigenvalue within delta: a certified, non-trivial parity shift (count k or n - k)
+        n = cloud.n
+        ks = list(range(1, ENDS + 1)) + list(range(n - ENDS + 1, n + 1))
+        t_loc = time.perf_counter()
+        ests = multisection(H, ks, iv, delta / 4, cache=InertiaCache(), batch=32)
+        t_loc = time.perf_counter() - t_loc
+        lam = {e.k: (e.value, e.half_width) for e in ests}
+        located = [[e.k, e.value, e.half_width] for e in ests]
+        print(name, "located", located, f"{t_loc:.1f}s", flush=True)
         mus, rejected = [], []
-        for q, m in enumerate(cands):
-            negs = [int(pc[3 * q + d, 0]) for d in range(3)]
-            ok = len(set(negs)) == 1 and 0 < negs[0] < cloud.n
-            (mus if ok else rejected).append(m)
-            print(name, "candidate", m, "negatives at -d/0/+d", negs, "ok" if ok else "", flush=True)
-        # prefer one from each end of the spectrum
-        if len(mus) > KEEP:
-            mus = [mus[0], mus[-1]]
+        for side in (range(1, ENDS), range(n - ENDS + 1, n)):
+            best = None
+            for k in side:
+                (a, ha), (b, hb) = lam[k], lam[k + 1]
+                gap = (b - hb) - (a + ha)
+                if gap > 3 * delta and (best is None or gap > best[0]):
+                    best = (gap, 0.5 * (a + ha + b - hb), k)
+            if best is not None:
+                mus.append(best[1])
+            else:
+                rejected.append(list(side))
+        # independent check of the certification: equal counts at mu - delta, mu, mu + delta
+        probe = [x for m in mus for x in (m - delta, m, m + delta)]
+        pc, _, _ = ldl_counts_array(H, probe) if probe else (np.zeros((0, 3)), None, None)
+        certified = [[int(pc[3 * q + d, 0]) for d in range(3)] for q in range(len(mus))]
+        print(name, "shifts", mus, "negatives at -d/0/+d", certified, flush=True)
         gpu = {}
-        for label, (mb, conc, sched, order, budget) in (
-                ("reference_order", (4, 1, 0, 1 if name == "cfg4" else 0, 0)),
-                ("production", PROD[name] + (1,))):
+        for label, (mb, conc, sched, order, budget, arith) in (
+                ("reference_order", (4, 1, 0, 1 if name == "cfg4" else 0, 0, 0)),
+                ("production", PROD[name] + (1, 1))):
+            eng.set_option("schur_arith", arith)
             eng.set_option("max_batch", mb)
             eng.set_option("concurrency", conc)
             eng.set_option("schedule", sched)
@@ -116,6 +130,7 @@ def main():
         except Exception:  # noqa: BLE001
             threads = os.cpu_count()
         rec = {"config": name, "n": cloud.n, "interval": list(iv), "mus": mus,
+               "located_eigenvalues": located, "locate_s": t_loc, "probe_negatives": certified,
                "guard_delta": delta, "rejected_candidates": rejected,
                "construct_device_s": t_con, "export_s": t_exp, "gpu": gpu, "oracle": cpu,
                "host_threads": threads, "cpu_count": os.cpu_count(),
