@@ -190,6 +190,7 @@ size_t schur_oz_scratch_bytes(int rows_total, int kpad, int nshift);
 cudaError_t launch_schur_oz(const OzJob *jobs, const int *row_job, const int2 *tile_ij,
                             int rows_total, int kpad, int total_tiles, int nshift, void *scratch,
                             cudaStream_t st, int probe = 0);
+void oz_prof_fetch(unsigned long long *out, bool reset);  // probe 8 phase counters (16 values)
 void launch_schur_sym(const double *X, const double *Bg, int64_t sx, int ld, int R, int K,
                       const int *seg_of, const int *seg_start, int nseg, const SchurTarget *tbl,
                       int nshift, cudaStream_t st, int variant = 0);

@@ -22,7 +22,7 @@
 //               double-buffered (2 x 96 KB);
 //   warp 1      TMEM allocation + MMA issue (one thread): 36 pairs x 2 K-steps of
 //               M=128, N=64, K=32 per stage, tcgen05.commit frees the stage;
-//   warps 2..9  epilogue: tcgen05.ld of the 8 group accumulators, fp64 sum, tile
+//   warps 4..11 epilogue: tcgen05.ld of the 8 group accumulators, fp64 sum, tile
 //               staged in shared memory, then the segment-pair scatter of
 //               schur_sym_kernel (fire-and-forget RED.ADD.F64, one writer per
 //               element), row-contiguous so a warp's reductions hit one row.
@@ -49,8 +49,8 @@ constexpr int STAGE = SLICES * (A_SLICE + B_SLICE);    // 48 KB
 constexpr int NSTAGE = 3;
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 64 + 32 * EPI_WARPS;           // 320
-constexpr int CT_LD = BN + 1;                          // staged tile row stride (doubles)
-constexpr int CT_BYTES = BM * CT_LD * 8;
+constexpr int PATCH_LD = 33;                           // staged 32 x 32 patch row stride (doubles)
+constexpr int CT_BYTES = EPI_WARPS * 32 * PATCH_LD * 8;  // one patch per epilogue warp
 constexpr int SMEM = NSTAGE * STAGE + CT_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
 // K-major operand tile with 32-byte swizzle: rows of 32 bytes (one K step), 8-row
@@ -132,11 +132,28 @@ __global__ void __launch_bounds__(256) oz_split_kernel(const OzJob *jobs, const 
 __device__ __forceinline__ double i2d_exact(int v) {
     return __hiloint2double(0x43380000 + (v >> 31), v) - 6755399441055744.0;
 }
+// exact int64 -> fp64 for |v| < 2^51, same trick in 64 bits
+__device__ __forceinline__ double i2d_exact64(long long v) {
+    return __longlong_as_double(0x4338000000000000LL + v) - 6755399441055744.0;
+}
+// -v 2^e on the integer pipe (v normal or zero; a result below the normal range is flushed
+// to zero: it is < 2^-1022 against targets of order one)
+__device__ __forceinline__ double neg_scale_pow2(double v, int e) {
+    const int hi = __double2hiint(v), lo = __double2loint(v);
+    const int ex = (hi >> 20) & 0x7ff;
+    const bool zero = ex == 0 || ex + e <= 0;
+    return __hiloint2double(zero ? 0 : (hi + (e << 20)) ^ 0x80000000, zero ? 0 : lo);
+}
 // 2^e (exact; fast path for the normal range)
 __device__ __forceinline__ double pow2i(int e) {
     return (e >= -1022 && e <= 1023) ? __longlong_as_double((long long)(e + 1023) << 52)
                                      : scalbn(1.0, e);
 }
+
+// probe 8 (diagnostic): cycles per phase, summed over CTAs.  0 items, 1 epilogue: segment
+// tables, 2 epilogue: wait for the MMAs, 3 TMEM read + group sum, 4 tile staging,
+// 5 scatter, 8 issuer: wait for the epilogue, 9 issuer: wait for TMA, 10 issuer: issue
+__device__ unsigned long long g_oz_prof[16];
 
 // Persistent: one CTA per SM walks the (shift, tile) items; the TMA producer and the
 // MMA issuer run ahead across items, the epilogue of item i overlaps the MMAs of
@@ -148,20 +165,18 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
                     const int *ex_all, const int *eb_all, int probe) {
     using namespace oz;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    // aligned by an offset (not a cast) so the compiler keeps the shared address space
+    unsigned char *smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
     double *ct = (double *)(smem + NSTAGE * STAGE);           // staged output tile
     uint64_t *full = (uint64_t *)(smem + NSTAGE * STAGE + CT_BYTES);
     uint64_t *empty = full + NSTAGE;
     uint64_t *tfull = empty + NSTAGE;
     uint64_t *tempty = tfull + 1;
     uint32_t *tmem_slot = (uint32_t *)(tempty + 1);
-    __shared__ int s_rseg[BM], s_roff[BM], s_cseg[BN], s_coff[BN], s_box[4];
-    constexpr int MAXT = 64;
-    __shared__ SchurTarget s_tbl[MAXT];
-    __shared__ double s_sr[BM], s_sc[BN];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int items = total_tiles * nshift;
+    const bool prof = probe == 8;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < NSTAGE; ++s) {
@@ -218,19 +233,23 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
     } else if (warp == 1) {
         if (lane == 0) {
             int kstep = 0, it = 0;
+            long long pm[3] = {0, 0, 0};
             for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
                 OzJob jb;
                 int z, m0, n0;
                 locate(item, jb, z, m0, n0);
                 const int nkb = (jb.K + BKB - 1) / BKB;
+                long long c0 = prof ? clock64() : 0;
                 mbar_wait(tempty, (it & 1) ^ 1);     // the epilogue has read the previous totals
                 tc_fence_after();
+                if (prof) { const long long c1 = clock64(); pm[0] += c1 - c0; c0 = c1; }
                 for (int kb = 0; kb < nkb; ++kb, ++kstep) {
                     const int s = kstep % NSTAGE;
                     // probe (benchmarking only): 1 = MMAs without waiting for the loads,
                     // 2 = loads without MMAs
                     if (probe != 1) mbar_wait(&full[s], (kstep / NSTAGE) & 1);
                     tc_fence_after();
+                    if (prof) { const long long c1 = clock64(); pm[1] += c1 - c0; c0 = c1; }
                     if (probe == 2) {
                         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[s])) : "memory");
                         continue;
@@ -252,122 +271,148 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
                         }
                     }
                     tc_commit(&empty[s]);
+                    if (prof) { const long long c1 = clock64(); pm[2] += c1 - c0; c0 = c1; }
                 }
                 tc_commit(tfull);
+            }
+            if (prof) {
+                atomicAdd(&g_oz_prof[8], (unsigned long long)pm[0]);
+                atomicAdd(&g_oz_prof[9], (unsigned long long)pm[1]);
+                atomicAdd(&g_oz_prof[10], (unsigned long long)pm[2]);
+                atomicAdd(&g_oz_prof[0], (unsigned long long)it);
             }
         }
     } else {
         // ---------------------------------------------------------- epilogue
+        // Eight independent warps, no barrier between them: warp (q, h) owns the 32 x 32
+        // patch of the tile at rows 32 q (its TMEM lane quadrant), columns 32 h.  Per item:
+        // the 8 group totals of its patch are read from tensor memory and summed (C), the
+        // patch is transposed through the warp's own shared-memory slab (D: row = TMEM
+        // lane -> row-contiguous lanes) and scattered to the target blocks as
+        // fire-and-forget L2 reductions, one writer per element per launch (E).  The
+        // segment data of the warp's rows / columns live in registers (lane = row, and
+        // lane = column) and are fetched one item ahead; since the warps drift apart,
+        // one warp's reductions drain while another converts.
+        // (tools/micro/scatter_bench.cu: reductions, load/add/store and TMA bulk reduce all
+        // run at the same HBM-bound rate for this traffic; only the reductions need no
+        // loads in flight.)
         const int q = warp & 3, h = (warp - 2) >> 2;       // TMEM lane quadrant, column half
-        const int rl = q * 32 + lane, t = threadIdx.x - 64, ew = warp - 2;
+        const int ew = warp - 2;
+        double *patch = ct + ew * (32 * PATCH_LD);
         int it = 0;
+        long long pe[5] = {0, 0, 0, 0, 0}, c0 = prof ? clock64() : 0;
+        auto tick = [&](int k) {
+            if (prof) { const long long c1 = clock64(); pe[k] += c1 - c0; c0 = c1; }
+        };
+        struct Seg {              // lane = row (r*) and lane = column (c*) of the patch
+            int rseg, roff, cseg, coff;
+            int er, ec;           // row / column scale exponents
+            SchurTarget e0;       // target of (first row segment, this lane's column segment)
+        };
+        auto fetch = [&](int item, Seg &sg) {
+            OzJob jb;
+            int z, m0, n0;
+            locate(item, jb, z, m0, n0);
+            const int gr = m0 + 32 * q + lane, gc = n0 + 32 * h + lane;
+            sg.rseg = gr < jb.R ? __ldg(jb.seg_of + gr) : -1;
+            sg.cseg = gc < jb.R ? __ldg(jb.seg_of + gc) : -1;
+            sg.roff = sg.rseg >= 0 ? gr - __ldg(jb.seg_start + sg.rseg) : 0;
+            sg.coff = sg.cseg >= 0 ? gc - __ldg(jb.seg_start + sg.cseg) : 0;
+            sg.er = __ldg(ex_all + (size_t)z * rows_total + jb.row0 + gr);
+            sg.ec = __ldg(eb_all + (size_t)z * rows_total + jb.row0 + gc);
+            const int a0 = __shfl_sync(0xffffffffu, sg.rseg, 0);
+            sg.e0 = SchurTarget{nullptr, 0, 0, 0};
+            if (a0 >= 0 && sg.cseg >= 0) sg.e0 = jb.tbl[(size_t)a0 * jb.nseg + sg.cseg];
+        };
+        Seg cur, nxt;
+        if ((int)blockIdx.x < items) fetch(blockIdx.x, cur);
         for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
             OzJob jb;
             int z, m0, n0;
             locate(item, jb, z, m0, n0);
-            // the previous item's scatter is done with the staged tile and tables
-            asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
-            for (int x = t; x < BM + BN; x += 32 * EPI_WARPS) {
-                const int g = x < BM ? m0 + x : n0 + (x - BM);
-                const int sg = g < jb.R ? jb.seg_of[g] : -1;
-                const int off = sg >= 0 ? g - jb.seg_start[sg] : 0;
-                if (x < BM) {
-                    s_rseg[x] = sg;
-                    s_roff[x] = off;
-                    s_sr[x] = pow2i(ex_all[(size_t)z * rows_total + jb.row0 + g]);
-                } else {
-                    s_cseg[x - BM] = sg;
-                    s_coff[x - BM] = off;
-                    s_sc[x - BM] = pow2i(eb_all[(size_t)z * rows_total + jb.row0 + g]);
-                }
-            }
-            asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
-            if (t == 0) {
-                const int rlast = min(BM, jb.R - m0) - 1, clast = min(BN, jb.R - n0) - 1;
-                s_box[0] = s_rseg[0];
-                s_box[1] = s_rseg[rlast] - s_rseg[0] + 1;
-                s_box[2] = s_cseg[0];
-                s_box[3] = s_cseg[clast] - s_cseg[0] + 1;
-            }
-            asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
-            const int alo = s_box[0], na = s_box[1], blo = s_box[2], nb = s_box[3];
-            const bool in_smem = na * nb <= MAXT;
-            if (in_smem)
-                for (int e = t; e < na * nb; e += 32 * EPI_WARPS)
-                    s_tbl[e] = jb.tbl[(size_t)(alo + e / nb) * jb.nseg + blo + e % nb];
-            asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
+            // the next item's segment data: the loads fly during this item's work
+            if (item + (int)gridDim.x < items) fetch(item + gridDim.x, nxt);
+            tick(0);
+            // ---- (C) group totals
             mbar_wait(tfull, it & 1);
             tc_fence_after();
+            tick(1);
+            // the 8 group totals are merged exactly in 64-bit integers three at a time
+            // (|total| < 2^31, so v0 2^14 + v1 2^7 + v2 < 2^46) before the fp64 sum: 3
+            // conversions and 3 fp64 terms per element instead of 8
             double acc[32];
 #pragma unroll
-            for (int c = 0; c < 32; ++c) acc[c] = 0.0;
-#pragma unroll 1
-            for (int g = SLICES - 1; g >= 0; --g) {
-                uint32_t v[32];
-                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + g * BN + h * 32, v);
-                const double w = pow2i(-7 * (g + 2));
+            for (int half = 0; half < 2; ++half) {
+                const uint32_t tcol = tmem + ((uint32_t)(q * 32) << 16) + h * 32 + half * 16;
+                uint32_t va[16], vb[16], vc[16];
+                tmem_ld16_nowait(tcol + 6 * BN, va);
+                tmem_ld16_nowait(tcol + 7 * BN, vb);
+                tmem_ld_wait();
 #pragma unroll
-                for (int c = 0; c < 32; ++c) acc[c] = fma(i2d_exact((int)v[c]), w, acc[c]);
+                for (int c = 0; c < 16; ++c)
+                    acc[half * 16 + c] =
+                        i2d_exact64(((long long)(int)va[c] << 7) + (int)vb[c]) * 0x1p-63;
+                tmem_ld16_nowait(tcol + 3 * BN, va);
+                tmem_ld16_nowait(tcol + 4 * BN, vb);
+                tmem_ld16_nowait(tcol + 5 * BN, vc);
+                tmem_ld_wait();
+#pragma unroll
+                for (int c = 0; c < 16; ++c)
+                    acc[half * 16 + c] = fma(i2d_exact64(((long long)(int)va[c] << 14) +
+                                                         ((long long)(int)vb[c] << 7) + (int)vc[c]),
+                                             0x1p-49, acc[half * 16 + c]);
+                tmem_ld16_nowait(tcol + 0 * BN, va);
+                tmem_ld16_nowait(tcol + 1 * BN, vb);
+                tmem_ld16_nowait(tcol + 2 * BN, vc);
+                tmem_ld_wait();
+#pragma unroll
+                for (int c = 0; c < 16; ++c)
+                    acc[half * 16 + c] = fma(i2d_exact64(((long long)(int)va[c] << 14) +
+                                                         ((long long)(int)vb[c] << 7) + (int)vc[c]),
+                                             0x1p-28, acc[half * 16 + c]);
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(tempty)) : "memory");
-            asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");  // tables ready
-            const double sr = s_sr[rl];
+            tick(2);
+            // ---- (D) transpose through the warp's slab
+            {
+                double *row = patch + lane * PATCH_LD;
 #pragma unroll
-            for (int c = 0; c < 32; ++c) ct[rl * CT_LD + h * 32 + c] = acc[c] * sr;
-            asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
-            // warp w: rows w, w + 8, ...; lane: columns lane, lane + 32 (row-contiguous
-            // REDs).  A lane's two columns are fixed for the tile: their segment, offset
-            // and scale are hoisted, and the target of (row segment, column segment) is
-            // re-read only when the row segment changes (a tile spans a few segments).
-            int cb2[2], bseg[2];
-            double sc2[2];
-            bool live[2];
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                const int cl = hh * 32 + lane;
-                bseg[hh] = s_cseg[cl];
-                cb2[hh] = s_coff[cl];
-                sc2[hh] = -s_sc[cl];
-                live[hh] = bseg[hh] >= 0;
+                for (int c = 0; c < 32; ++c) row[c] = acc[c];
             }
-            int a_cur = -1;
-            double *tb[2] = {nullptr, nullptr};
-            int64_t tld[2] = {0, 0};
-            bool ttr[2] = {false, false}, mir[2] = {false, false};
-            for (int r = ew; r < BM; r += EPI_WARPS) {
-                const int gr = m0 + r, a = s_rseg[r], ra = s_roff[r];
-                if (a < 0) break;
-                if (a != a_cur) {
-                    a_cur = a;
-#pragma unroll
-                    for (int hh = 0; hh < 2; ++hh) {
-                        tb[hh] = nullptr;
-                        if (!live[hh]) continue;
-                        const int b = bseg[hh];
-                        const SchurTarget e = in_smem ? s_tbl[(a - alo) * nb + (b - blo)]
-                                                      : jb.tbl[(size_t)a * jb.nseg + b];
-                        if (!e.base) continue;
-                        tb[hh] = e.base + z * e.bs;
-                        tld[hh] = e.ldc;
-                        ttr[hh] = e.trans != 0;
-                        mir[hh] = a == b;
+            __syncwarp();
+            tick(3);
+            // ---- (E) row j of the patch -> one row-contiguous reduction per lane
+            if (probe != 4) {
+                const bool live = cur.cseg >= 0;
+                const int gc = n0 + 32 * h + lane, cb = cur.coff, b = cur.cseg;
+                int a_cur = __shfl_sync(0xffffffffu, cur.rseg, 0);
+                SchurTarget e = cur.e0;
+#pragma unroll 4
+                for (int j = 0; j < 32; ++j) {
+                    const int a = __shfl_sync(0xffffffffu, cur.rseg, j);
+                    const int ra = __shfl_sync(0xffffffffu, cur.roff, j);
+                    const int er = __shfl_sync(0xffffffffu, cur.er, j);
+                    if (a < 0) break;
+                    if (a != a_cur) {
+                        a_cur = a;
+                        if (live) e = jb.tbl[(size_t)a * jb.nseg + b];
                     }
-                }
-                if (probe == 4) continue;  // benchmarking only: no reductions
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                    const int cl = hh * 32 + lane;
-                    if (!tb[hh] || n0 + cl < gr) continue;
-                    const double val = ct[r * CT_LD + cl] * sc2[hh];
-                    const int cb = cb2[hh];
-                    red_add_f64(tb[hh] + (ttr[hh] ? (int64_t)cb * tld[hh] + ra : (int64_t)ra * tld[hh] + cb),
-                                val);
-                    if (mir[hh] && cb != ra && probe != 3) red_add_f64(tb[hh] + (int64_t)cb * tld[hh] + ra, val);
+                    if (!live || !e.base || gc < m0 + 32 * q + j) continue;
+                    const double val = neg_scale_pow2(patch[j * PATCH_LD + lane], er + cur.ec);
+                    double *tb = e.base + z * e.bs;
+                    const int64_t tld = e.ldc;
+                    red_add_f64(tb + (e.trans ? (int64_t)cb * tld + ra : (int64_t)ra * tld + cb), val);
+                    if (a == b && cb != ra && probe != 3) red_add_f64(tb + (int64_t)cb * tld + ra, val);
                 }
             }
+            __syncwarp();
+            cur = nxt;
+            tick(4);
         }
+        if (prof && ew == 0 && lane == 0)
+            for (int k = 0; k < 5; ++k) atomicAdd(&g_oz_prof[1 + k], (unsigned long long)pe[k]);
     }
     tc_fence_before();
     __syncthreads();
@@ -410,6 +455,14 @@ cudaError_t make_map(CUtensorMap *m, const int8_t *base, int kpad, int rows, int
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 }  // namespace
+
+void oz_prof_fetch(unsigned long long *out, bool reset) {
+    cudaMemcpyFromSymbol(out, g_oz_prof, sizeof(g_oz_prof));
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(g_oz_prof, z, sizeof(z));
+    }
+}
 
 size_t schur_oz_scratch_bytes(int rows_total, int kpad, int nshift) {
     const size_t sl = (size_t)oz::SLICES * rows_total * kpad * nshift;
@@ -461,6 +514,8 @@ cudaError_t launch_schur_oz(const OzJob *jobs, const int *row_job, const int2 *t
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
+    static const int env_probe = getenv("H2L_OZ_PROBE") ? atoi(getenv("H2L_OZ_PROBE")) : 0;
+    if (!probe) probe = env_probe;
     const int items = total_tiles * nshift;
     schur_oz_kernel<<<items < nsm ? items : nsm, oz::THREADS, oz::SMEM, st>>>(
         mx, mb, jobs, tile_ij, total_tiles, nshift, rows_total, exr, ebr, probe);

@@ -358,6 +358,11 @@ extern "C" int h2l_internal_schur_oz(int device, int R, int K, int nshift, const
     });
 }
 
+// phase counters of schur_oz_kernel under probe 8 (H2L_OZ_PROBE=8 in the engine)
+extern "C" int h2l_internal_oz_prof(unsigned long long *out16, int reset) {
+    return guarded(nullptr, [&] { h2l::oz_prof_fetch(out16, reset != 0); });
+}
+
 // ---- tcgen05 INT8 MMA issue-rate probe: one CTA per SM issues `count` MMAs of shape
 // M=128 x N=n x K=32 (SWIZZLE_32B K-major operands, zeroed shared memory) from one
 // thread and reports cycles per MMA.  order 0: runs of 8 MMAs into the same

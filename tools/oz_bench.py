@@ -30,3 +30,10 @@ for (s, R, K) in [(7, 4096, 448), (7, 16384, 160), (7, 16384, 256), (2, 40960, 1
         fl = s * R * (R + 1) * K
         print(f"probe={pr} s={s} R={R} K={K}: {ms.value:.3f} ms  {fl / ms.value / 1e9:.1f} TF/s "
               f"fp64-equivalent", flush=True)
+        if pr == 8:
+            buf = (ctypes.c_ulonglong * 16)()
+            lib.h2l_internal_oz_prof(buf, 1)
+            v = list(buf)
+            names = ["items", "epi:tables", "epi:wait_mma", "epi:tmem+sum", "epi:stage", "epi:scatter", "",
+                     "", "mma:wait_epi", "mma:wait_tma", "mma:issue"]
+            print("   cycles per item:", {n: round(v[k] / max(1, v[0])) for k, n in enumerate(names) if n and k})

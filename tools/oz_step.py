@@ -27,3 +27,14 @@ for rep in range(2):
           f"schur {stt['ms_schur']:.1f} ms ({stt['schur_flops'] / stt['ms_schur'] / 1e9:.1f} TF/s), "
           f"launches {stt['launches']}", flush=True)
 print(counts[:, 0].tolist())
+if os.environ.get("H2L_OZ_PROBE") == "8":
+    import ctypes
+    tl = _native.load_testing_library()
+    buf = (ctypes.c_ulonglong * 16)()
+    tl.h2l_internal_oz_prof(buf, 1)
+    v = list(buf)
+    items = max(1, v[0])
+    names = ["items", "epi:tables", "epi:wait_mma", "epi:tmem+sum", "epi:stage", "epi:scatter", "", "",
+             "mma:wait_epi", "mma:wait_tma", "mma:issue"]
+    print("oz phases (cycles per item):",
+          {n: round(v[k] / items) for k, n in enumerate(names) if n and k}, "items", items)
