@@ -128,6 +128,8 @@ public:
         else if (k == "elim_order") elim_order_ = (int)v;
         else if (k == "qr_budget") qr_budget_ = v != 0;
         else if (k == "block_cache") block_cache_ = v != 0;
+        else if (k == "block_classes") block_classes_ = v != 0;
+        else if (k == "block_cache_mb") bcache_cap_ = std::max<int64_t>(0, v) << 20;
         else if (k == "schedule") schedule_ = (int)std::max<int64_t>(0, std::min<int64_t>(3, v));
         else if (k == "window") window_ = (int)std::max<int64_t>(1, v);
         else if (k == "group_mem_mb") group_mem_mb_ = std::max<int64_t>(1, v);
@@ -258,7 +260,7 @@ public:
         ranges_ = o.ranges_; boff_ = o.boff_; brank_ = o.brank_; bdim_ = o.bdim_;
         dense_ = o.dense_; lowrank_ = o.lowrank_; deferred_ = o.deferred_; coup_off_ = o.coup_off_;
         arena_ = o.arena_; skel_ = o.skel_; skel_diag_ = o.skel_diag_; skel_off_ = o.skel_off_;
-        max_batch_ = o.max_batch_; time_kernels_ = o.time_kernels_; schedule_ = o.schedule_; window_ = o.window_; group_mem_mb_ = o.group_mem_mb_; group_max_ = o.group_max_; elim_order_ = o.elim_order_; qr_budget_ = o.qr_budget_; block_cache_ = o.block_cache_; schur_arith_ = o.schur_arith_;
+        max_batch_ = o.max_batch_; time_kernels_ = o.time_kernels_; schedule_ = o.schedule_; window_ = o.window_; group_mem_mb_ = o.group_mem_mb_; group_max_ = o.group_max_; elim_order_ = o.elim_order_; qr_budget_ = o.qr_budget_; block_cache_ = o.block_cache_; block_classes_ = o.block_classes_; bcache_cap_ = o.bcache_cap_; schur_arith_ = o.schur_arith_;
         owns_payload_ = false;
         uploaded_ = o.uploaded_;
     }
@@ -544,6 +546,37 @@ private:
         static const bool on = getenv("H2L_HOSTPROF") != nullptr;
         return on;
     }
+    // H2L_HOSTPROF host-time buckets: 0 pool alloc, 1 pool free, 2 schedule, 3 BK setup,
+    // 4 panel segments, 5 panel solve / GEMM task lists, 6 Schur tables (incl. fill creation),
+    // 7 Schur staging + launch, 8 compaction, 9 task-list flushes
+    double hp_ms_[12] = {};
+    long long hp_n_[12] = {};
+    int hp_cur_ = -1;
+    std::chrono::steady_clock::time_point hp_t_;
+    void hp_switch(int k) {   // sequential sections: time since the last switch goes to the last bucket
+        if (!hostprof_on()) return;
+        const auto now = std::chrono::steady_clock::now();
+        if (hp_cur_ >= 0) {
+            hp_ms_[hp_cur_] += std::chrono::duration<double, std::milli>(now - hp_t_).count();
+            hp_n_[hp_cur_]++;
+        }
+        hp_cur_ = k;
+        hp_t_ = now;
+    }
+    struct HostTimer {
+        Wave *w;
+        int k;
+        std::chrono::steady_clock::time_point t0;
+        HostTimer(Wave *w_, int k_) : w(hostprof_on() ? w_ : nullptr), k(k_) {
+            if (w) t0 = std::chrono::steady_clock::now();
+        }
+        ~HostTimer() {
+            if (w) {
+                w->hp_ms_[k] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+                w->hp_n_[k]++;
+            }
+        }
+    };
 
     // debug (H2L_DEBUG_GUARD): every block gets GUARD doubles of 0xff canary on both
     // sides, checked after every launch by dbg_sync()
@@ -585,14 +618,23 @@ private:
                 b.p = base + GUARD;
                 live_[b.p] = inner;
             } else {
-                const int64_t nd = b.bs * s_;
+                const int64_t nd = size_class(b.bs * s_);
                 auto it = block_cache_ ? bcache_.find(nd) : bcache_.end();
                 if (it != bcache_.end() && !it->second.empty()) {
                     b.p = it->second.back();
                     it->second.pop_back();
                     bcache_bytes_ -= nd * (int64_t)sizeof(double);
                 } else {
-                    CK(cudaMallocFromPoolAsync((void **)&b.p, sizeof(double) * nd, pool_, st_));
+                    HostTimer ht(this, 0);
+                    cudaError_t e = cudaMallocFromPoolAsync((void **)&b.p, sizeof(double) * nd, pool_, st_);
+                    if (e == cudaErrorMemoryAllocation && bcache_bytes_ > 0) {
+                        // the cached free blocks are the only memory this wave can give back
+                        cudaGetLastError();
+                        flush_block_cache();
+                        CK(cudaStreamSynchronize(st_));
+                        e = cudaMallocFromPoolAsync((void **)&b.p, sizeof(double) * nd, pool_, st_);
+                    }
+                    CK(e);
                 }
             }
             if (zero) CK(cudaMemsetAsync(b.p, 0, sizeof(double) * b.bs * s_, st_));
@@ -610,18 +652,30 @@ private:
                 // same-size blocks are re-issued from a host-side free list (one stream:
                 // stream order makes reuse safe); the pool call per block costs more
                 // host time than the kernels of small fronts
-                const int64_t nd = b.bs * s_, by = nd * (int64_t)sizeof(double);
-                if (block_cache_ && bcache_bytes_ + by <= BCACHE_CAP) {
+                const int64_t nd = size_class(b.bs * s_), by = nd * (int64_t)sizeof(double);
+                if (block_cache_ && bcache_bytes_ + by <= bcache_cap_) {
                     bcache_[nd].push_back(b.p);
                     bcache_bytes_ += by;
                 } else {
+                    HostTimer ht(this, 1);
                     CK(cudaFreeAsync(b.p, st_));
                 }
             }
         }
         b = Blk{};
     }
-    static constexpr int64_t BCACHE_CAP = int64_t(2) << 30;
+    // Blocks are allocated in size classes (8 per octave: <= 12.5 % slack) so that the
+    // blocks a moving front retires (compaction shrinks every block of an eliminated
+    // cluster) are re-issued to the blocks it creates: on config 4 (~1M block
+    // allocations per wave) the pool calls were most of the step's host time.
+    int64_t bcache_cap_ = int64_t(2) << 30;
+    int block_classes_ = 1;
+    int64_t size_class(int64_t nd) const {
+        if (!block_classes_ || nd <= 64) return nd;
+        int lg = 63 - __builtin_clzll((unsigned long long)nd);
+        const int64_t step = int64_t(1) << (lg - 3);
+        return (nd + step - 1) / step * step;
+    }
     std::unordered_map<int64_t, std::vector<double *>> bcache_;
     int64_t bcache_bytes_ = 0;
     bool block_cache_ = true;
@@ -767,6 +821,7 @@ private:
                   int64_t *dev_out) {
         const auto wall0 = std::chrono::steady_clock::now();
         wait_ms_ = host_rec_ms_ = host_elim_ms_ = 0.0;
+        for (int q = 0; q < 12; ++q) hp_ms_[q] = 0.0, hp_n_[q] = 0;
         s_ = s;
         st_acc_ = &acc;
         ev_used_ = 0;
@@ -858,6 +913,14 @@ private:
                     "host in recompress %.1f ms (incl. syncs), in eliminate %.1f ms\n", s,
                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count(),
                     wait_ms_, host_rec_ms_, host_elim_ms_);
+        if (hostprof_on()) {
+            static const char *nm[12] = {"pool_alloc", "pool_free", "schedule", "bk_setup", "panel_segs",
+                                         "panel_tasks", "schur_tables", "schur_launch", "compaction",
+                                         "flushes", "", ""};
+            fprintf(stderr, "hostprof buckets (ms, calls):");
+            for (int q = 0; q < 10; ++q) fprintf(stderr, " %s %.1f (%lld)", nm[q], hp_ms_[q], hp_n_[q]);
+            fprintf(stderr, "\n");
+        }
         st_acc_ = nullptr;
     }
 
@@ -1110,7 +1173,11 @@ private:
     void process_level(int level) {
         const bool leaf = level == depth_;
         t_level_max_ = -1;
-        const auto groups = make_schedule(level);
+        std::vector<std::vector<int>> groups;
+        {
+            HostTimer ht(this, 2);
+            groups = make_schedule(level);
+        }
         st_acc_->groups += (int64_t)groups.size();
         for (const auto &g : groups) {
             if (leaf && (npend_ || npend_diag_)) {
@@ -1639,6 +1706,7 @@ private:
         if (J.empty()) return;
         // ---- K2/K3: BK of D[:nR,:nR] with fused inertia (packed triangle in one CTA's
         // shared memory, or in a thread-block cluster's distributed shared memory)
+        hp_switch(3);
         {
             std::vector<BkJob> small, big;
             int nsmall = 0, nbig = 0;
@@ -1675,6 +1743,7 @@ private:
             dbg_sync("bk");
         }
         // ---- panel segments (live rows only)
+        hp_switch(4);
         for (auto &j : J) {
             const int i = j.i;
             Blk &D = diag_[i];
@@ -1697,6 +1766,7 @@ private:
                 j.R += g.len;
             }
         }
+        hp_switch(5);
         // ---- K4/K5: the panel solve on the nR x nR identity: W_I = P^T L^{-T}, X_I =
         // W_I D^{-1} (the reference: dtrsm + dgesv on Ball, gldl.py:372-378); then
         // G = X_I W_I^T = P^T L^{-T} D^{-1} L^{-1} P and X = Bg G on the tensor pipe
@@ -1761,6 +1831,7 @@ private:
                     add_gemm(g1, gm(j.Bg.p, j.Bg.bs, j.nR, 0, j.G.p, j.G.bs, j.nR, 0, j.Xb.p, j.Xb.bs,
                                     j.nR, j.R, j.nR, j.nR, 1.0, 0.0), s_);
             flush(g1, s_);
+            hp_switch(6);
             // ---- K6: C_big -= X Bg^T over the upper triangle of every job's R x R panel
             // space, scattered to the target blocks (fill blocks created on demand,
             // zeroed in one batched launch first: gldl.py:398-409)
@@ -1854,6 +1925,7 @@ private:
                 st_acc_->gemm_flops_exec += oz ? 2.0 * (double)tl * 128 * 64 * ((nR + 63) / 64 * 64) * s_
                                                : 2.0 * (double)tl * 64 * 64 * nR * s_;
             }
+            hp_switch(7);
             flush(fz);
             // one staged region: segment maps, target tables, tile->job map, job table
             // (whose pointers into the same region are patched on the host first)
@@ -1923,8 +1995,10 @@ private:
                     kmax = std::max(kmax, q.K);
                     fl += (double)q.R * q.R * q.K;
                 }
-                fprintf(stderr, "schurlog arith=%d jobs=%zu Rmax=%d Kmax=%d tiles=%d shifts=%d ms=%.3f tflops=%.1f\n",
-                        (int)oz, sj.size(), rmax, kmax, tiles_tot, s_, ms, fl * s_ / (ms * 1e-3) / 1e12);
+                fprintf(stderr, "schurlog arith=%d jobs=%zu Rmax=%d Kmax=%d tiles=%d shifts=%d ms=%.3f tflops=%.1f "
+                                "alg_bytes=%.0f\n",
+                        (int)oz, sj.size(), rmax, kmax, tiles_tot, s_, ms, fl * s_ / (ms * 1e-3) / 1e12,
+                        bytes_tot * s_);
                 cudaEventDestroy(lg0);
                 cudaEventDestroy(lg1);
             }
@@ -1941,6 +2015,7 @@ private:
         // columns (the R part is zero from now on and never read again), and i
         // becomes an m = nS, nR = 0 cluster: later panels, Schur targets, merges and
         // fill blocks see only live rows, and the front's memory shrinks as it moves.
+        hp_switch(8);
         {
             CopyBatch zc;
             std::vector<std::pair<Blk *, Blk>> repl;
@@ -1981,6 +2056,7 @@ private:
             CK(cudaFreeAsync(j.perm, st_));
             CK(cudaFreeAsync(j.dinfo, st_));
         }
+        hp_switch(-1);
     }
 
     void bk_launch(double *a, int64_t astride, int ld, int n, int *perm, double *dinfo, int64_t ps) {

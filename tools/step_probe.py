@@ -29,7 +29,7 @@ def main():
     eng = _native.engine_for(H, 0)
     a, b = iv
     mus = [a + (b - a) * (j + 1) / (S + 1) for j in range(S)]
-    ref = None
+    ref = counts = status = None
     for opts in os.environ.get("OPTS", "").split(";"):
         for kv in filter(None, opts.split(",")):
             k, v = kv.split("=")
@@ -54,7 +54,8 @@ def main():
             elif not np.array_equal(ref, counts):
                 print(f"[{opts}] COUNTS DIFFER: {np.nonzero((ref != counts).any(axis=1))[0].tolist()}",
                       flush=True)
-    print("neg counts", counts[:, 0].tolist(), "status", status.tolist(), flush=True)
+    if counts is not None:
+        print("neg counts", counts[:, 0].tolist(), "status", status.tolist(), flush=True)
 
 
 if __name__ == "__main__":
