@@ -582,13 +582,16 @@ def run_ours(args):
         dist.destroy_process_group()
         return
     traffic = None
-    try:  # DRAM bytes per Schur launch from the committed ncu --set full capture (config 2)
-        with open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")) as f:
+    # DRAM bytes per Schur launch from the committed ncu --set full capture of one config-2
+    # wave with the arithmetic in use (tools/ncu_traffic.py)
+    tfile = "r2_ncu_traffic.json" if arith == 1 else "r1_ncu_traffic.json"
+    try:
+        with open(os.path.join(ROOT, "profiles", tfile)) as f:
             tr = json.load(f)
         if wl.name == "cfg2":
             traffic = {"dram_bytes_per_launch": tr["dram_bytes_per_launch_mean"],
                        "algorithmic_bytes_per_launch": tr["algorithmic_bytes_per_launch_mean"],
-                       "source": "profiles/r1_ncu_traffic.json"}
+                       "kernel": tr.get("kernel"), "source": "profiles/" + tfile}
     except (OSError, KeyError, ValueError):
         pass
     line = {

@@ -91,12 +91,17 @@ __global__ void __launch_bounds__(256) oz_split_kernel(const OzJob *jobs, const 
     const int z = blockIdx.y, which = blockIdx.z;
     const OzJob jb = jobs[row_job[row / oz::BM]];
     const int r = row - jb.row0;
-    int8_t *out = (which ? sb_out : sx_out) + ((size_t)z * oz::SLICES * rows_total + row) * kpad;
+    // slice plane layout [K block of 32 bytes][row][32]: the 128 (64) rows of one K block
+    // of a tile are one contiguous 4 KB (2 KB) run, so the TMA fetches whole 128-byte lines
+    // instead of one 32-byte sector per row
     const size_t plane = (size_t)rows_total * kpad;
+    int8_t *out = (which ? sb_out : sx_out) + (size_t)z * oz::SLICES * plane + (size_t)row * oz::BKB;
+    const size_t kbs = (size_t)rows_total * oz::BKB;   // bytes between K blocks
     int *eo = (which ? eb_out : ex_out) + (size_t)z * rows_total + row;
     if (r >= jb.R) {
         for (int p = 0; p < oz::SLICES; ++p)
-            for (int k = lane * 4; k < kpad; k += 128) *(int *)(out + p * plane + k) = 0;
+            for (int k = lane * 4; k < kpad; k += 128)
+                *(int *)(out + p * plane + (k / oz::BKB) * kbs + (k % oz::BKB)) = 0;
         if (lane == 0) *eo = 0;
         return;
     }
@@ -122,7 +127,7 @@ __global__ void __launch_bounds__(256) oz_split_kernel(const OzJob *jobs, const 
                 v[q] = t - d;                        // exact: the remaining bits
                 packed |= ((uint32_t)(uint8_t)(int8_t)(int)d) << (8 * q);
             }
-            *(uint32_t *)(out + p * plane + k0) = packed;
+            *(uint32_t *)(out + p * plane + (k0 / oz::BKB) * kbs + (k0 % oz::BKB)) = packed;
         }
     }
 }
@@ -222,9 +227,9 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
                     mbar_expect_tx(&full[s], STAGE);
                     unsigned char *a = smem + s * STAGE, *b = a + SLICES * A_SLICE;
                     for (int p = 0; p < SLICES; ++p) {
-                        tma_load_3d(a + p * A_SLICE, &map_x, &full[s], kb * BKB, jb.row0 + m0,
+                        tma_load_4d(a + p * A_SLICE, &map_x, &full[s], 0, jb.row0 + m0, kb,
                                     z * SLICES + p);
-                        tma_load_3d(b + p * B_SLICE, &map_b, &full[s], kb * BKB, jb.row0 + n0,
+                        tma_load_4d(b + p * B_SLICE, &map_b, &full[s], 0, jb.row0 + n0, kb,
                                     z * SLICES + p);
                     }
                 }
@@ -445,11 +450,13 @@ cudaError_t make_map(CUtensorMap *m, const int8_t *base, int kpad, int rows, int
                      int box_rows) {
     EncodeTiled fn = encode_fn();
     if (!fn) return cudaErrorNotSupported;
-    cuuint64_t dims[3] = {(cuuint64_t)kpad, (cuuint64_t)rows, (cuuint64_t)planes};
-    cuuint64_t strides[2] = {(cuuint64_t)kpad, (cuuint64_t)kpad * rows};
-    cuuint32_t box[3] = {(cuuint32_t)oz::BKB, (cuuint32_t)box_rows, 1};
-    cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void *)base, dims, strides, box, es,
+    // [plane][K block][row][32 bytes]
+    cuuint64_t dims[4] = {(cuuint64_t)oz::BKB, (cuuint64_t)rows, (cuuint64_t)(kpad / oz::BKB),
+                          (cuuint64_t)planes};
+    cuuint64_t strides[3] = {(cuuint64_t)oz::BKB, (cuuint64_t)oz::BKB * rows, (cuuint64_t)kpad * rows};
+    cuuint32_t box[4] = {(cuuint32_t)oz::BKB, (cuuint32_t)box_rows, 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, (void *)base, dims, strides, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
