@@ -395,7 +395,9 @@ def run_ours(args):
     eng.set_option("max_batch", (S + conc - 1) // conc)
     eng.set_option("concurrency", conc)
     wl.config["waves"] = f"{conc} concurrent wave(s) of <= {(S + conc - 1) // conc} shifts"
-    sched = args.schedule if args.schedule >= 0 else (1 if wl.name in ("cfg1", "cfg2") else 2)
+    # config 5: colour classes of 64-cluster windows (a moving front: the plain colour
+    # schedule keeps every leaf block materialised and two waves of 8 exceed 180 GB)
+    sched = args.schedule if args.schedule >= 0 else {"cfg1": 1, "cfg2": 1, "cfg5": 3}.get(wl.name, 2)
     eng.set_option("schedule", sched)
     arith = args.schur_arith if args.schur_arith >= 0 else DEFAULT_SCHUR_ARITH
     eng.set_option("schur_arith", arith)
@@ -403,7 +405,8 @@ def run_ours(args):
                                      1: "fp64-accurate Ozaki slices on INT8 tcgen05"}[arith]
     wl.config["schedule"] = {0: "one cluster at a time, ascending (the reference)",
                              1: "ascending-order wavefronts (level-batched, reference order)",
-                             2: "colour classes (level-batched, re-ordered)"}[sched]
+                             2: "colour classes (level-batched, re-ordered)",
+                             3: "colour classes of 64-cluster windows (level-batched, re-ordered)"}[sched]
     if wl.name == "cfg4":
         # the unit-sphere front does not fit one B200 in the reference's ascending
         # order; low-degree-first keeps a shift at ~45 GB.  A re-ordering changes fills and

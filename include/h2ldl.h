@@ -187,10 +187,11 @@ int h2l_comm_destroy(h2l_comm *comm);
  *                 rank (+32) pivots, redone with all pivots when the rank reaches
  *                 the budget (same rank as the full ordering; the dropped
  *                 complement gets a different orthonormal basis), 0 full ordering;
- *  "block_cache"  1/0 host free list of retired blocks, re-issued to new blocks of the same
- *                 size class; "block_classes" 1 (default): sizes rounded up to 8 classes per
- *                 octave (<= 12.5 % slack), 0: exact sizes; "block_cache_mb": cap of the
- *                 list (default 2048);
+ *  "block_cache"  how working blocks are allocated: 2 (default) from a host-side arena
+ *                 (large slabs of the wave's pool, best-fit free list with coalescing),
+ *                 1 from free lists of retired blocks per size class ("block_classes" 1:
+ *                 8 classes per octave, 0: exact sizes; "block_cache_mb": cap, default
+ *                 2048), 0 one stream-ordered pool call per block;
  *  "schur_arith"  arithmetic of the Schur update (the dominant kernel): 0 fp64 on the
  *                 DMMA pipe (mma.sync), 1 (default) fp64-accurate on the INT8 tensor cores
  *                 (tcgen05.mma.kind::i8): each row of X / Bg split into 8 exact

@@ -127,7 +127,7 @@ public:
         else if (k == "borrow_arena") borrow_arena_ = v != 0;
         else if (k == "elim_order") elim_order_ = (int)v;
         else if (k == "qr_budget") qr_budget_ = v != 0;
-        else if (k == "block_cache") block_cache_ = v != 0;
+        else if (k == "block_cache") block_cache_ = (int)std::max<int64_t>(0, std::min<int64_t>(2, v));
         else if (k == "block_classes") block_classes_ = v != 0;
         else if (k == "block_cache_mb") bcache_cap_ = std::max<int64_t>(0, v) << 20;
         else if (k == "schedule") schedule_ = (int)std::max<int64_t>(0, std::min<int64_t>(3, v));
@@ -271,8 +271,10 @@ public:
         cudaSetDevice(dev_);
         cudaStreamSynchronize(st_);
         cudaGetLastError();
+        const bool in_arena = !guard_mode() && !barena_.slabs.empty();
         auto drop = [&](Blk &b) {
-            if (b.p) cudaFreeAsync(guard_mode() ? b.p - GUARD : b.p, st_);
+            if (b.p && !(in_arena && barena_.live.count((char *)b.p)))
+                cudaFreeAsync(guard_mode() ? b.p - GUARD : b.p, st_);
             b = Blk{};
         };
         for (auto &b : diag_) drop(b);
@@ -285,6 +287,7 @@ public:
             for (double *p : kv.second) cudaFreeAsync(p, st_);
         bcache_.clear();
         bcache_bytes_ = 0;
+        arena_release_all(false);
         release_oz_scratch();
         for (void *p : {(void *)d_mu_, (void *)d_tol_, (void *)d_dropped_, (void *)d_counts_,
                         (void *)d_status_, (void *)d_rank_})
@@ -604,6 +607,91 @@ private:
             }
         }
     }
+    // ---- block arena (block_cache = 2, default): working blocks are carved out of large
+    // slabs by a best-fit free list with coalescing, on the host.  A config-4 wave makes
+    // ~1.7M block allocations and as many frees (every elimination compacts every block
+    // of the cluster); through the stream-ordered pool that was half of the wave's wall
+    // time.  One stream per wave makes the reuse of a freed range stream-ordered.
+    struct Arena {
+        static constexpr size_t SLAB = size_t(512) << 20, GRAN = 256;
+        std::vector<std::pair<char *, size_t>> slabs;
+        std::map<char *, size_t> by_addr;                 // free ranges
+        std::set<std::pair<size_t, char *>> by_size;
+        std::unordered_map<char *, size_t> live;
+        void erase_free(std::map<char *, size_t>::iterator it) {
+            by_size.erase({it->second, it->first});
+            by_addr.erase(it);
+        }
+        void add_free(char *p, size_t n) {
+            auto nx = by_addr.lower_bound(p);
+            if (nx != by_addr.end() && p + n == nx->first) {   // merge with the next range
+                n += nx->second;
+                auto dead = nx++;
+                erase_free(dead);
+            }
+            if (nx != by_addr.begin()) {                        // merge with the previous one
+                auto pv = std::prev(nx);
+                if (pv->first + pv->second == p) {
+                    p = pv->first;
+                    n += pv->second;
+                    erase_free(pv);
+                }
+            }
+            by_addr.emplace_hint(nx, p, n);
+            by_size.emplace(n, p);
+        }
+        char *take(size_t n) {                                   // nullptr: no free range fits
+            auto it = by_size.lower_bound({n, nullptr});
+            if (it == by_size.end()) return nullptr;
+            char *p = it->second;
+            const size_t have = it->first;
+            by_addr.erase(p);
+            by_size.erase(it);
+            if (have > n) {
+                by_addr[p + n] = have - n;
+                by_size.emplace(have - n, p + n);
+            }
+            live[p] = n;
+            return p;
+        }
+        void give(char *p) {
+            auto it = live.find(p);
+            if (it == live.end()) return;
+            const size_t n = it->second;
+            live.erase(it);
+            add_free(p, n);
+        }
+    } barena_;
+    double *arena_alloc(int64_t nd) {
+        const size_t n = ((size_t)nd * sizeof(double) + Arena::GRAN - 1) / Arena::GRAN * Arena::GRAN;
+        char *p = barena_.take(n);
+        if (!p) {
+            // a new slab; its last GRAN bytes are never handed out, so ranges of two slabs
+            // are never adjacent and never merge
+            HostTimer ht(this, 0);
+            size_t want = std::max(n, Arena::SLAB);
+            char *base = nullptr;
+            cudaError_t e = cudaMallocFromPoolAsync((void **)&base, want + Arena::GRAN, pool_, st_);
+            if (e == cudaErrorMemoryAllocation && want > n) {
+                cudaGetLastError();
+                want = n;
+                e = cudaMallocFromPoolAsync((void **)&base, want + Arena::GRAN, pool_, st_);
+            }
+            CK(e);
+            barena_.slabs.emplace_back(base, want + Arena::GRAN);
+            barena_.add_free(base, want);
+            p = barena_.take(n);
+        }
+        return (double *)p;
+    }
+    void arena_release_all(bool throwing = true) {
+        for (auto &sl : barena_.slabs) {
+            cudaError_t e = cudaFreeAsync(sl.first, st_);
+            if (throwing) CK(e);
+        }
+        barena_ = Arena{};
+    }
+
     Blk alloc(int rows, int cols, bool zero) {
         Blk b;
         b.rows = rows;
@@ -617,6 +705,8 @@ private:
                 CK(cudaMemsetAsync(base, 0xff, sizeof(double) * (inner + 2 * GUARD), st_));
                 b.p = base + GUARD;
                 live_[b.p] = inner;
+            } else if (block_cache_ == 2) {
+                b.p = arena_alloc(b.bs * s_);
             } else {
                 const int64_t nd = size_class(b.bs * s_);
                 auto it = block_cache_ ? bcache_.find(nd) : bcache_.end();
@@ -648,6 +738,8 @@ private:
                 check_guards();
                 live_.erase(b.p);
                 CK(cudaFreeAsync(b.p - GUARD, st_));
+            } else if (block_cache_ == 2) {
+                barena_.give((char *)b.p);
             } else {
                 // same-size blocks are re-issued from a host-side free list (one stream:
                 // stream order makes reuse safe); the pool call per block costs more
@@ -678,7 +770,7 @@ private:
     }
     std::unordered_map<int64_t, std::vector<double *>> bcache_;
     int64_t bcache_bytes_ = 0;
-    bool block_cache_ = true;
+    int block_cache_ = 2;   // 0 pool call per block, 1 free lists per size class, 2 arena
     void flush_block_cache() {
         for (auto &kv : bcache_)
             for (double *p : kv.second) CK(cudaFreeAsync(p, st_));
@@ -900,6 +992,7 @@ private:
             for (int z = 0; z < s; ++z) status[z] = hs[z] ? H2L_SHIFT_SINGULAR : H2L_SHIFT_OK;
         }
         release_oz_scratch();
+        arena_release_all();
         for (double *p : {d_mu_, d_tol_, d_dropped_}) CK(cudaFreeAsync(p, st_));
         CK(cudaFreeAsync(d_counts_, st_));
         CK(cudaFreeAsync(d_status_, st_));

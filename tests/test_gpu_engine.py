@@ -303,7 +303,7 @@ def test_engine_options_keep_counts(option):
     schedule) never change the inertia: counts equal the reference's with the
     option off and on, on instances with recompression and merges."""
     names = [n for n in instance_names() if n.startswith("mini")] + ["circle256_h2_e8"]
-    values = {"qr_budget": (0, 1), "block_cache": (0, 1), "block_classes": (0, 1),
+    values = {"qr_budget": (0, 1), "block_cache": (0, 1, 2), "block_classes": (0, 1),
               "schedule": (0, 2, 1)}[option]
     for name in names:
         H = h2matrix.load_payload(f"tests/golden/h_{name}.npz")
@@ -316,5 +316,5 @@ def test_engine_options_keep_counts(option):
                 assert not status.any(), (name, option, v)
                 assert np.array_equal(counts, z["counts"]), (name, option, v)
         finally:
-            eng.set_option(option, {"qr_budget": 1, "block_cache": 1, "block_classes": 1,
+            eng.set_option(option, {"qr_budget": 1, "block_cache": 2, "block_classes": 1,
                                     "schedule": 1}[option])

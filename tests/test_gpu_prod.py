@@ -43,7 +43,7 @@ PRODUCTION = {
     "cfg2": (7, 1, 1, 0),
     "cfg3": (8, 2, 2, 0),
     "cfg4": (2, 1, 2, 1),
-    "cfg5": (8, 2, 2, 0),
+    "cfg5": (8, 2, 3, 0),
 }
 
 _cache = {}
