@@ -387,11 +387,13 @@ def run_ours(args):
     _native.set_default_device(local)
     wl = make_workload(args.config)
     H = wl.H
-    S = args.batch or {"cfg1": 255, "cfg2": 7, "cfg4": 2}.get(wl.name, 15)
+    S = args.batch or {"cfg1": 255, "cfg2": 7, "cfg4": 4}.get(wl.name, 15)
     eng = _native.engine_for(H, local)
     # latency-bound configs overlap two waves' per-cluster chains (tools/conc_sweep.py:
     # config 3 0.24 vs 0.27 s per shift); config 2 is memory- and DMMA-bound
-    conc = 2 if wl.name in ("cfg3", "cfg5") else 1
+    # (config 4: 42 GB per wave of 2 shifts, and the host work of its ~590k fill blocks is
+    # as long as its kernels: a second wave on its own host thread overlaps the two)
+    conc = 2 if wl.name in ("cfg3", "cfg4", "cfg5") else 1
     eng.set_option("max_batch", (S + conc - 1) // conc)
     eng.set_option("concurrency", conc)
     wl.config["waves"] = f"{conc} concurrent wave(s) of <= {(S + conc - 1) // conc} shifts"
@@ -452,10 +454,22 @@ def run_ours(args):
 
     # warm-up: W rounds of a search for another index (restarted if it converges)
     k_warm = wl.ks[0] if wl.ks[0] != wl.k else wl.n + 1 - wl.k
+    from paper_2311_08618_b200.errors import NativeError
+
     try:
         while True:
-            multisection(H, [k_warm], wl.interval, wl.eps_ev, cache=InertiaCache(),
-                         batch=S * world, evaluate=evaluate)
+            try:
+                multisection(H, [k_warm], wl.interval, wl.eps_ev, cache=InertiaCache(),
+                             batch=S * world, evaluate=evaluate)
+            except NativeError as exc:
+                # the working set of `conc` waves did not fit this device: one wave at a time
+                if conc == 1 or "memory" not in str(exc):
+                    raise
+                conc = 1
+                eng.set_option("concurrency", 1)
+                wl.config["waves"] = f"1 wave of <= {(S + 1) // 2} shifts at a time (two did not fit)"
+                state["n"] = 0
+                del steps[:]
     except _Stop:
         pass
     # timed: exactly K rounds; fresh searches for k (then the config's other indices,
