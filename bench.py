@@ -668,6 +668,20 @@ def _ref_cfg1_worker(args):
     return [engine_ref.inertia(H, float(mu), skel_cache=cache) for mu in mus]
 
 
+def _ref_cfg1_slice_worker(args):
+    """One complete bisection (the oracle's restatement of slice_spectrum) at one BLAS thread."""
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    k, interval, eps_ev = args
+    from paper_2311_08618_b200 import configs, construct
+    from oracle import engine_ref
+
+    cloud, kern, tree, st = configs.config_problem("cfg1", seed=0)
+    H = construct(kern, tree, st, configs.CONFIGS["cfg1"].eps)
+    t0 = time.perf_counter()
+    val, hw, it, evals, _ = engine_ref.slice_spectrum(H, k, interval, eps_ev, skel_cache={})
+    return k, val, it, evals, time.perf_counter() - t0
+
+
 def _dyadic_round(interval, q):
     a, b = interval
     pts = []
@@ -700,6 +714,23 @@ def run_reference(args):
             for _ in range(K):
                 pool.map(_ref_cfg1_worker, [([rng.uniform(lo, hi)],) for _ in range(cores)])
             dt = time.perf_counter() - t0
+            # the full slice_spectrum(k = n/2) at one BLAS thread, and
+            # the static partition -- one index per worker, `cores` workers at one thread each
+            eigs = z["eigs"]
+            k0 = 1024
+            one = pool.map(_ref_cfg1_slice_worker, [(k0, (lo, hi), EPS_EV)])[0]
+            t0 = time.perf_counter()
+            part = pool.map(_ref_cfg1_slice_worker,
+                            [(k0 - cores // 2 + w, (lo, hi), EPS_EV) for w in range(cores)])
+            t_part = time.perf_counter() - t0
+        extra = {"slice_spectrum_1_thread": {"k": k0, "seconds": one[4], "inertia_evals": one[3],
+                                             "iterations": one[2], "evals_per_s": one[3] / one[4],
+                                             "abs_err_vs_eigvalsh": abs(one[1] - float(eigs[k0 - 1]))},
+                 "static_partition": {"workers": cores, "blas_threads_per_worker": 1,
+                                      "eigenvalues": len(part), "wall_s": t_part,
+                                      "eigenvalues_per_s": len(part) / t_part,
+                                      "max_abs_err_vs_eigvalsh": max(abs(p[1] - float(eigs[p[0] - 1]))
+                                                                     for p in part)}}
         v = cores * K / dt
         step_ms = 1e3 * dt / K
         units_per_step = cores
@@ -753,6 +784,7 @@ def run_reference(args):
         cfg = dict(wl.config)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "cfg1_eigenvalue_runs": locals().get("extra"),
         "steps": K, "warmup": W, "ms_per_step": step_ms, "evaluations_per_step": units_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": cfg,
