@@ -387,13 +387,14 @@ def run_ours(args):
     _native.set_default_device(local)
     wl = make_workload(args.config)
     H = wl.H
-    S = args.batch or {"cfg1": 255, "cfg2": 7, "cfg4": 4}.get(wl.name, 15)
+    # S = 2^q - 1: one multisection round resolves q bisection levels
+    S = args.batch or {"cfg1": 255, "cfg2": 7, "cfg4": 3}.get(wl.name, 15)
     eng = _native.engine_for(H, local)
     # latency-bound configs overlap two waves' per-cluster chains (tools/conc_sweep.py:
     # config 3 0.24 vs 0.27 s per shift); config 2 is memory- and DMMA-bound
-    # (config 4: 42 GB per wave of 2 shifts, and the host work of its ~590k fill blocks is
-    # as long as its kernels: a second wave on its own host thread overlaps the two)
-    conc = 2 if wl.name in ("cfg3", "cfg4", "cfg5") else 1
+    # (config 4: ~21 GB per shift next to 65 GB of payload: one wave of 3 shifts; two
+    # concurrent waves of 2 do not fit)
+    conc = 2 if wl.name in ("cfg3", "cfg5") else 1
     eng.set_option("max_batch", (S + conc - 1) // conc)
     eng.set_option("concurrency", conc)
     wl.config["waves"] = f"{conc} concurrent wave(s) of <= {(S + conc - 1) // conc} shifts"
