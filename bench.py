@@ -392,12 +392,13 @@ def run_ours(args):
     eng = _native.engine_for(H, local)
     # latency-bound configs overlap two waves' per-cluster chains (tools/conc_sweep.py:
     # config 3 0.24 vs 0.27 s per shift); config 2 is memory- and DMMA-bound
-    # (config 4: ~21 GB per shift next to 65 GB of payload: one wave of 3 shifts; two
-    # concurrent waves of 2 do not fit)
     conc = 2 if wl.name in ("cfg3", "cfg5") else 1
-    eng.set_option("max_batch", (S + conc - 1) // conc)
+    # config 4: ~21 GB per shift next to 65 GB of payload -- a round's 3 shifts run as waves
+    # of 2 + 1 (three at once, or two concurrent waves, do not fit 180 GB)
+    per_wave = 2 if wl.name == "cfg4" else (S + conc - 1) // conc
+    eng.set_option("max_batch", per_wave)
     eng.set_option("concurrency", conc)
-    wl.config["waves"] = f"{conc} concurrent wave(s) of <= {(S + conc - 1) // conc} shifts"
+    wl.config["waves"] = f"{conc} concurrent wave(s) of <= {per_wave} shifts"
     # config 5: colour classes of 64-cluster windows (a moving front: the plain colour
     # schedule keeps every leaf block materialised and two waves of 8 exceed 180 GB)
     sched = args.schedule if args.schedule >= 0 else {"cfg1": 1, "cfg2": 1, "cfg5": 3}.get(wl.name, 2)
@@ -542,8 +543,10 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    # (at most the first 4 timed rounds: the replay costs as much as the rounds themselves)
+    e2e_mus = timed_mus[:4]
     t0 = time.perf_counter()
-    for mus in timed_mus:
+    for mus in e2e_mus:
         inertia_batch(H, mus)
     torch.cuda.synchronize()
     t_e2e = time.perf_counter() - t0
@@ -551,7 +554,8 @@ def run_ours(args):
         tt = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_e2e = float(tt.item())
-    e2e = n_all / t_e2e if t_e2e > 0 else None
+    n_e2e = sum(len(m) for m in e2e_mus) * world
+    e2e = n_e2e / t_e2e if t_e2e > 0 else None
     # ---- eigenvalue: projection from the measured rounds; --eig runs the search
     q = max(1, int(math.floor(math.log2(S * world + 1))))
     levels, nrounds = rounds_needed(wl.interval, wl.eps_ev, q)
@@ -573,8 +577,7 @@ def run_ours(args):
     if wl.name == "cfg2" and world == 1 and not args.no_batch32:
         mus32 = np.linspace(wl.interval[0], wl.interval[1], 34)[1:33]
         _, _, st32 = ldl_counts_array(H, mus32)
-        batched32 = {"shifts": 32, "max_batch": (S + conc - 1) // conc,
-                     "waves": -(-32 // ((S + conc - 1) // conc)),
+        batched32 = {"shifts": 32, "max_batch": per_wave, "waves": -(-32 // per_wave),
                      "ms_total": st32["ms_total"], "value": 32 / (st32["ms_total"] / 1e3),
                      "unit": UNIT, "mem_peak_gb_per_wave": st32["mem_peak"] / 1e9,
                      "note": "32 shifts exceed one B200 as a single wave (~16 GB each): one "
@@ -629,7 +632,7 @@ def run_ours(args):
                                                "recompression_ordering"], kinds)) if kinds else None,
                        "device_mem_peak_gb": mem_peak / 1e9},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * S,
-                "d2h_bytes_per_step": (3 * 8 + 4) * S},
+                "d2h_bytes_per_step": (3 * 8 + 4) * S, "steps_replayed": len(e2e_mus)},
         "gpu_launches": launches,
         "clocks": clk,
         "single_shift": {"value": single_rate, "unit": UNIT, "ms_per_step": float(np.mean(single))},

@@ -42,7 +42,7 @@ NAMES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, 
 PRODUCTION = {
     "cfg2": (7, 1, 1, 0),
     "cfg3": (8, 2, 2, 0),
-    "cfg4": (3, 1, 2, 1),
+    "cfg4": (2, 1, 2, 1),
     "cfg5": (8, 2, 3, 0),
 }
 

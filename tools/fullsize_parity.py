@@ -25,7 +25,7 @@ import numpy as np  # noqa: E402
 # than the parity guard DELTA); counts there are non-trivial (k and n - k negatives)
 ENDS = 4
 GUARD = 10.0  # DELTA = GUARD * eps * max(|lo|, |hi|): the guard of the reference fixtures
-PROD = {"cfg2": (7, 1, 1, 0), "cfg3": (8, 2, 2, 0), "cfg4": (3, 1, 2, 1), "cfg5": (8, 2, 3, 0)}
+PROD = {"cfg2": (7, 1, 1, 0), "cfg3": (8, 2, 2, 0), "cfg4": (2, 1, 2, 1), "cfg5": (8, 2, 3, 0)}
 
 
 def main():
