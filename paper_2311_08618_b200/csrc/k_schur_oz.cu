@@ -2,7 +2,7 @@
 // fp64-accurate by exact integer slicing (the Ozaki scheme).
 //
 // Blackwell has no fp64 tcgen05 kind; the fp64 path is DMMA through mma.sync at
-// ~37 TF/s (k_gemm.cu schur_sym_kernel).  The INT8 tensor pipe is 4.5 POPS dense.
+// ~37 TF/s (k_gemm.cu schur_sym_kernel).  The INT8 tensor pipe is 4.5 POPS dense nominal (cuBLASLt measures 3.0-3.1).
 // Every row r of X (and of Bg) is written exactly as
 //     x_rk = 2^e_r * sum_{p<8} 2^{-7(p+1)} s_rkp ,   s_rkp in [-127, 127]
 // (e_r = exponent of the row's largest entry; each slice peels 7 bits; the residual
@@ -11,21 +11,29 @@
 // product exact in int32 (|sum| <= 127^2 K < 2^31 for K <= 2^17).  Pairs with
 // i + j <= 7 are kept (36 of 64; the dropped tail is < 2^-63 of the row/column
 // maxima), and all pairs of one i + j = g share one int32 accumulator in tensor
-// memory: 8 groups x 64 columns = the SM's 512 TMEM columns.  The epilogue sums
-// the 8 group totals in fp64 (smallest first) and applies the row/column exponents;
-// the only roundings are those of that final 8-term fp64 sum -- fewer than the
-// K-term fp64 dot product of the DMMA kernel.
+// memory: 8 groups x 64 columns = the SM's 512 TMEM columns.  The epilogue merges
+// the 8 group totals exactly in int64, three at a time, sums the three fp64 terms
+// (smallest first) and applies the row/column exponents; the only roundings are
+// those of that final three-term sum -- fewer than the K-term fp64 dot product of
+// the DMMA kernel.
 //
-// Kernel structure (one CTA per 128 x 64 upper-triangle tile x shift, 1 CTA/SM):
-//   warp 0      TMA producer: per 64-byte K block, the 8 slices of the X rows
-//               (8 x 128 x 64 B) and of the Bg rows (8 x 64 x 64 B), SWIZZLE_64B,
-//               double-buffered (2 x 96 KB);
-//   warp 1      TMEM allocation + MMA issue (one thread): 36 pairs x 2 K-steps of
-//               M=128, N=64, K=32 per stage, tcgen05.commit frees the stage;
-//   warps 4..11 epilogue: tcgen05.ld of the 8 group accumulators, fp64 sum, tile
-//               staged in shared memory, then the segment-pair scatter of
-//               schur_sym_kernel (fire-and-forget RED.ADD.F64, one writer per
-//               element), row-contiguous so a warp's reductions hit one row.
+// Kernel structure (persistent: one CTA of 10 warps per SM walks (shift, tile) items;
+// tile = 128 x 64 of a cluster's upper triangle, fixed by the 512 TMEM columns):
+//   warp 0      TMA producer: per 32-byte K block the 8 slices of 128 X rows and of 64 Bg
+//               rows (8 x 4 KB + 8 x 2 KB = 48 KB, SWIZZLE_32B), 3 stages, running ahead
+//               across items; the slice planes are stored [K block][row][32 bytes], so
+//               a box is one contiguous run;
+//   warp 1      TMEM allocation + MMA issue (one thread): slice i of X against the
+//               stacked slices [T_0 .. T_{7-i}] of Bg -- 12 wide MMAs (N <= 256) per K
+//               step land all 36 pairs in the accumulators of their groups;
+//               tcgen05.commit frees the stage;
+//   warps 2..9  eight independent epilogue warps (no barrier between them): warp (q, h)
+//               owns the 32 x 32 patch at TMEM lane quadrant q, column half h -- tcgen05.ld
+//               of its 8 group totals, exact int64 merge, fp64 sum, release of tensor
+//               memory, transpose through its own shared-memory slab, scatter to the
+//               target blocks as fire-and-forget RED.ADD.F64 (one writer per element per
+//               launch), row-contiguous.  Segment data live in registers, fetched one
+//               item ahead; power-of-two scales are applied on the integer pipe.
 // Reference: the Schur update of the elimination, gldl.py:388-409.
 #include <cuda.h>
 #include <cstdio>
