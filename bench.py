@@ -585,6 +585,9 @@ def run_ours(args):
     if args.eig:
         eng.set_option("time_kernels", 0)
         ks = list(wl.ks)
+        if args.eig_count and len(ks) > args.eig_count:   # the middle `eig_count` indices of the list
+            lo = (len(ks) - args.eig_count) // 2
+            ks = ks[lo:lo + args.eig_count]
         ev = sharded if world > 1 else (lambda mus: local_eval(mus))
         state["phase"] = "eig"
         if world > 1:
@@ -809,6 +812,8 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg1", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--batch", type=int, default=0, help="shifts per GPU per step")
     ap.add_argument("--eig", action="store_true", help="run the eigenvalue searches to the end")
+    ap.add_argument("--eig-count", type=int, default=0,
+                    help="with --eig: only the middle N indices of the config's k list")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
