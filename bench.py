@@ -12,23 +12,26 @@ Gershgorin row sums of the kernel matrix (gpu_build.gershgorin_device).
 
 A step is one batched sweep of the generalized LDL^T over the S shifts of one
 multisection round for k = n/2 (the shifts the eigenvalue search actually
-visits, starting from the Gershgorin interval: rounds 1..W are the warm-up,
-rounds W+1..W+K are timed).  `value` = shifts factorized per second over the K
+visits, starting from the Gershgorin interval: W warm-up rounds of a search for
+another index, then exactly K timed rounds of fresh searches for k, cycling over
+the config's k list).  `value` = shifts factorized per second over the K
 timed steps: device time (CUDA events on the engine stream around every
 h2l_inertia call), max over ranks.  The uploaded H (12.3 GB) and the per-shift
 working blocks (~16 GB per shift) are resident in HBM and exceed L2 by
 two orders of magnitude, so no flush is needed.  S defaults to 7 for cfg2: one
 3-level multisection round, the most shifts whose working set fits the GPU
-at once (BASELINE's "32 shifts per factorization" needs ~520 GB); `single_shift`
-reports the one-shift-per-step rate for comparison.
+at once (BASELINE's "32 shifts per factorization" needs ~520 GB: `batched_32`
+runs them as 5 consecutive waves inside one call); `single_shift` reports the
+one-shift-per-step rate for comparison.
 
-`e2e` replays the K timed shift lists through the public API
+`e2e` replays the first (at most 4) timed shift lists through the public API
 `inertia_batch(H, mus)` (host shifts in, host InertiaCount out, the engine's
 pinned H2D/D2H copies inside the timed region; wall clock).
 
-`eigenvalue`: seconds per k-th eigenvalue.  By default projected from the
-measured step times (rounds needed = ceil(log2(width/eps_ev) / 3)); with
---eig the multisection search for k in {1, n/2, n} runs to completion.
+`eigenvalue`: seconds per k-th eigenvalue, measured whenever a search completes
+inside the K timed rounds (config 2: 15 rounds), else projected from the measured
+step times and labelled so; with --eig the multisection search for the config's
+k list (or its middle --eig-count indices) runs to completion after the timed region.
 
 Multi-GPU (torchrun): one rank per GPU, each with a replica of H; a round has
 S x N shifts sharded over the ranks and one NCCL all-gather of the integer
@@ -36,12 +39,16 @@ counts (multigpu.ShardedEvaluator) -- weak scaling in shifts per step.
 
 `cpu_baseline` / `--impl reference`: the reference algorithm on the host
 through the oracle port (oracle/engine_ref.py) on the same H (exported to
-host memory), BLAS threads = all host cores.  A cfg2 factorization takes
-about an hour on the CPU, so each sample is the first T seconds of one
-factorization: its elimination flops (survey §8d count, the oracle tallies
-them) divided by the flops of a whole factorization (`elim_flops` of the
-device run, or profiles/r1_cfg2_workload.json for the reference arm) scale
-the sample to evaluations/s.
+host memory), BLAS threads = all host cores.  A complete cfg2 factorization
+takes 12-14 minutes on the box's 16 threads (measured:
+profiles/r2_cpu_full_evaluations.json, reported as `full_evaluation_measured`),
+so each sample is the first T seconds of one factorization: its elimination
+flops (survey 8d count, the oracle tallies them) divided by the flops of a
+whole factorization (`elim_flops` of the device run, or
+profiles/r1_cfg2_workload.json for the reference arm) scale the sample to
+evaluations/s (`extrapolated: true`).  `--impl reference --config cfg1` runs
+whole factorizations, the full slice_spectrum at one BLAS thread and the static
+partition over all cores.
 """
 
 import argparse
